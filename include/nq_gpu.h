@@ -1,0 +1,193 @@
+/*
+ * nq_gpu.h — C ABI of the B200-native N-Queens counting path (libnqb200.so).
+ *
+ * The reference (/root/reference/proj/include/nqueens/) is a header-only C++ library
+ * with no FFI. Its hot path is
+ *
+ *   execute(n, R, opts)               scheduler.hpp:573   generate + execute_batch
+ *   execute_batch(n, R, batch, opts)  scheduler.hpp:446   worker pool over count_with
+ *   count_with(variant, n, sub, cfg)  solver.hpp:350      one subproblem, CPU DFS
+ *   for_each_subproblem / generate    subproblems.hpp:80  folded frontier
+ *   count_subproblems                 subproblems.hpp:118
+ *
+ * This header is the plain-pointer boundary those entry points are re-bound to: the
+ * C++ drop-in headers in include/nqueens/ and the Python package call only these
+ * functions. Every entry point returns NQ_OK (0) or a negative status; the message of
+ * the last failure on the calling thread is nq_last_error():
+ *
+ *   NQ_ECUDA     (-1)  CUDA / device failure           ~ std::runtime_error
+ *   NQ_ECONFIG   (-2)  bad n / R / depth / input        ~ nqueens::config_error
+ *   NQ_EOVERFLOW (-3)  64-bit count overflow            ~ std::overflow_error
+ *   NQ_ECANCEL   (-4)  cancelled between chunks         (SolveReport::completed=false)
+ *
+ * There is no CPU fallback: every counting entry point runs the sm_100a kernels and
+ * fails with NQ_ECUDA when no device is usable.
+ */
+#ifndef NQ_GPU_H
+#define NQ_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NQ_OK 0
+#define NQ_ECUDA (-1)
+#define NQ_ECONFIG (-2)
+#define NQ_EOVERFLOW (-3)
+#define NQ_ECANCEL (-4)
+
+#define NQ_ABI_VERSION 1
+
+/* Packed 16-byte frontier record (one LDG.128 per refill on the device).
+ *   cols      occupied columns of the first placed_rows rows   (Subproblem::cur)
+ *   diag      left-diagonal threats shifted to the next row    (Subproblem::left)
+ *   antidiag  right-diagonal threats shifted to the next row   (Subproblem::right)
+ *   row       placed_rows | multiplier << 8                    (Subproblem::placed_rows,
+ *                                                              Subproblem::multiplier)
+ * Reference struct: solver.hpp:18-26 (20 bytes, int fields). */
+typedef struct nq_sub {
+  uint32_t cols, diag, antidiag, row;
+} nq_sub;
+
+/* Kernel variants of solver.hpp:28 (KernelVariant). Both run the same sm_100a DFS; the
+ * variant selects the feasibility rule (required_depth, stack_config.hpp:43-45) and
+ * which loop the reported node count follows (Alg. 2 or Alg. 3 iterations). */
+#define NQ_VARIANT_ITERATIVE 0
+#define NQ_VARIANT_LASTROW 1
+
+typedef struct nq_result {
+  uint64_t solutions;       /* Σ multiplier × count (checked on the host)           */
+  uint64_t raw_solutions;   /* Σ count, unweighted                                   */
+  uint64_t nodes;           /* DFS nodes: Alg. 3 (last-row) loop iterations           */
+  uint64_t iterations;      /* device loop iterations actually executed               */
+  uint64_t subproblems;     /* records processed                                      */
+  double kernel_ms;         /* device time of the counting kernel(s), CUDA events     */
+  double h2d_ms;            /* host→device copy time (0 for device-resident input)    */
+} nq_result;
+
+typedef struct nq_ctx nq_ctx; /* one per device; used by one host thread at a time */
+
+int nq_abi_version(void);
+const char* nq_last_error(void);
+int nq_device_count(int* out);
+
+/* --- per-device contexts --------------------------------------------------------- */
+int nq_ctx_create(int device, nq_ctx** out);
+void nq_ctx_destroy(nq_ctx* ctx);
+/* Tuning knobs (0 = default): threads per block, resident blocks per SM cap,
+ * dispatch order (0 = as given, 1 = reversed: the expensive tail of the DFS order
+ * first). */
+int nq_ctx_set_tuning(nq_ctx* ctx, int block, int blocks_per_sm, int reverse_order);
+
+/* Count a batch held in HOST memory (caller-owned, pageable or pinned). Synchronous.
+ * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:499-506).
+ * pre_rows is the batch's pre-placement depth R: it sizes the shared-memory stack
+ * (n-1-R frames, the Alg. 3 depth of stack_config.hpp:43-45); a record with fewer
+ * placed rows than R, cols outside the board, or popcount(cols) != placed_rows is
+ * rejected with NQ_ECONFIG naming its index. */
+int nq_count(nq_ctx* ctx, int n, int pre_rows, int variant, const nq_sub* host_subs,
+             uint64_t count, nq_result* out);
+/* Count a batch already resident in device memory of ctx's device. Synchronous. */
+int nq_count_device(nq_ctx* ctx, int n, int pre_rows, int variant, const nq_sub* dev_subs,
+                    uint64_t count, nq_result* out);
+/* Asynchronous form of nq_count_device: enqueue on the context stream; nq_collect
+ * waits and fills out. At most one batch in flight per context. */
+int nq_count_device_async(nq_ctx* ctx, int n, int pre_rows, int variant,
+                          const nq_sub* dev_subs, uint64_t count);
+int nq_collect(nq_ctx* ctx, nq_result* out);
+
+/* Per-subproblem results (unweighted counts, high-water marks as in
+ * KernelResult, solver.hpp:34-41, and Alg. 3 node counts). Host buffers. This is the
+ * count_with seam (solver.hpp:350) batched onto the device. */
+int nq_count_each(nq_ctx* ctx, int n, int pre_rows, int variant, const nq_sub* host_subs,
+                  uint64_t count, uint64_t* counts, int32_t* high_water, uint64_t* nodes);
+
+/* --- frontier (host C++, multi-threaded, deterministic reference order) ------------ */
+/* subproblems.hpp:80-115. out may be NULL (count only); writes min(cap, total). */
+int nq_generate(int n, int pre_rows, nq_sub* out, uint64_t cap, uint64_t* total);
+/* Systematic slice of the same stream: records with index ≡ offset (mod stride). */
+int nq_generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
+                      uint64_t cap, uint64_t* total);
+/* subproblems.hpp:118-145 */
+int nq_count_subproblems(int n, int pre_rows, uint64_t* total);
+
+/* --- partitions (scheduler.hpp:241-282) ----------------------------------------------- */
+/* ranges receives worker_count (first, last) pairs. */
+int nq_partition_uniform(uint64_t task_count, int worker_count, uint64_t* ranges);
+int nq_partition_weighted(uint64_t task_count, const double* weights, int worker_count,
+                          uint64_t* ranges);
+
+/* --- multi-GPU execution (scheduler.hpp:446 / :573) -------------------------------- */
+#define NQ_PARTITION_UNIFORM 0  /* PartitionStrategy::uniform  (scheduler.hpp:26)        */
+#define NQ_PARTITION_WEIGHTED 1 /* PartitionStrategy::weighted                          */
+#define NQ_PARTITION_STEALING 2 /* PartitionStrategy::stealing: fixed chunks, cursor    */
+#define NQ_PARTITION_GUIDED 3   /* GPU default: shrinking chunks, expensive end first   */
+
+#define NQ_LOG_GENERATION 0 /* "Use %.2fms to generate %llu subproblems!"               */
+#define NQ_LOG_START 1      /* "worker [%d] start job, with %llu(%.2f) subproblems."     */
+#define NQ_LOG_FINISH 2     /* "worker [%d] finish job."                                 */
+#define NQ_LOG_RESULT 3     /* "n %d queens result %llu, calc time: [%.2f ms]"           */
+
+/* Formats one timestamped log line of scheduler.hpp:163-203 into buf (NUL-terminated).
+ * kind NQ_LOG_GENERATION: (ms, count); START: (worker, count, fraction);
+ * FINISH: (worker); RESULT: (n, total, ms). Unused arguments are ignored. */
+int nq_format_log(int kind, int i, uint64_t u, double d, char* buf, uint64_t cap);
+
+typedef void (*nq_log_fn)(void* user, const char* line);
+
+typedef struct nq_solve_opts {
+  int variant;                 /* NQ_VARIANT_*                                          */
+  int strategy;                /* NQ_PARTITION_*                                        */
+  int worker_count;            /* workers; 0 = one per device. Worker w runs on          */
+                               /* devices[w % n_devices] with its own stream             */
+  const double* weights;       /* weighted: worker_count weights (NULL = equal)          */
+  uint64_t chunk;              /* stealing: records per chunk; guided: minimum chunk     */
+  int n_devices;               /* 0 = all visible                                        */
+  const int* devices;          /* optional explicit device list (length n_devices)       */
+  const volatile int* cancel;  /* non-zero → stop between chunks (completed = 0)         */
+  int stack_depth;             /* StackConfig::max_depth() of the caller's config; 0 = off */
+  const char* config_name;     /* for the require_feasible message                        */
+  nq_log_fn log;               /* optional start/finish line sink (called concurrently) */
+  void* log_user;
+} nq_solve_opts;
+
+#define NQ_MAX_WORKERS 64
+
+typedef struct nq_worker_stats {
+  int worker;
+  int device;
+  uint64_t assigned;           /* contiguous strategies: range size; 0 = dynamic        */
+  uint64_t processed;          /* records counted by this worker                        */
+  uint64_t partial_sum;        /* multiplier-weighted (checked)                         */
+  uint64_t nodes;              /* Alg. 3 nodes                                          */
+  uint64_t chunks;             /* kernel launches                                       */
+  double elapsed_ms;           /* host wall time of this worker thread                  */
+  double kernel_ms;            /* Σ device time of its launches                         */
+} nq_worker_stats;
+
+typedef struct nq_report {
+  uint64_t total;              /* multiplier-weighted solution count                    */
+  uint64_t task_count;
+  uint64_t nodes;
+  double generation_ms;
+  double calc_ms;              /* wall time of the device phase (excl. generation)      */
+  int completed;
+  int worker_count;
+  nq_worker_stats workers[NQ_MAX_WORKERS];
+} nq_report;
+
+int nq_solve_batch(int n, int pre_rows, const nq_sub* host_subs, uint64_t count,
+                   const nq_solve_opts* opts, nq_report* out);
+int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out);
+
+/* --- diagnostics ------------------------------------------------------------------- */
+/* Integer-pipe peak of the current device (LOP3+IMAD 1:1 stream, all SMs), thread
+ * ops/s and the SM clock seen; the roofline denominator of bench.py. */
+int nq_measure_int_peak(int device, double* ops_per_s, double* sm_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,26 @@
+// nq_internal.h — shared helpers of libnqb200.so (not installed).
+#pragma once
+#include <cstdint>
+#include <string>
+
+#include "nq_gpu.h"
+
+namespace nqb200 {
+
+// Records the thread-local message returned by nq_last_error(); returns code.
+int set_error(int code, const std::string& msg);
+
+int check_plan(int n, int pre_rows);
+int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
+                   uint64_t cap, uint64_t* total);
+int count_subproblems(int n, int pre_rows, uint64_t* total);
+
+// require_feasible (stack_config.hpp:59-71): the caller's stack budget must hold the
+// required depth n - R - lastrow; the message names the smallest built-in config.
+int require_feasible(int stack_depth, const char* config_name, int n, int pre_rows,
+                     bool last_row);
+
+// Index (within the last batch) of the record a counting call rejected, or ~0.
+uint64_t ctx_last_bad(const nq_ctx* c);
+
+}  // namespace nqb200

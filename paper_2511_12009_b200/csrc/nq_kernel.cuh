@@ -1,0 +1,248 @@
+// nq_kernel.cuh — the sm_100a persistent DFS counting kernel.
+//
+// Replaces the reference's per-subproblem CPU search (count_iterative_lastrow,
+// solver.hpp:295-348, called once per subproblem from execute_batch,
+// scheduler.hpp:499-506) with one persistent kernel that owns the whole batch.
+//
+// Execution model:
+//   * one subproblem per thread; a grid of (#SM x resident blocks) threads stays
+//     resident and refills idle lanes from a global atomic dispatch cursor, one
+//     atomicAdd per warp per refill round (ballot -> leader atomic -> shfl);
+//   * the CURRENT row's state (free columns C, diagonals l/r, untried candidates a)
+//     lives in registers; only rows with untried candidates left are pushed, as one
+//     16-byte frame, onto a per-thread stack in shared memory laid out interleaved
+//     (level L of thread t at frame index L*BLOCK + t), so that every LDS.128/STS.128
+//     quarter-warp touches 32 distinct banks whatever depth each lane is at;
+//   * the loop body is branch-free: push, descend, stay and pop are predicated;
+//     the popcount of Alg. 3's last-row test is replaced by "no free column left"
+//     (the LOP3 zero flag), because POPC issues at 1/4 of the ALU rate on sm_100;
+//   * an exhausted lane pops the level-0 sentinel frame and becomes idle-stable
+//     (a == 0 disables every side effect), so the idle check runs once per K steps;
+//   * per-lane u32 counters are folded into u64 totals at subproblem end and every
+//     2^16 K-step blocks, then warp-shuffle reduced with one atomicAdd per warp.
+//
+// Node accounting: one loop iteration places one queen at rows placed..n-1. The
+// reference's Alg. 3 settles row n-1 by popcount instead, so its iteration count is
+// ours minus the number of (unweighted) solutions; both are reported.
+#pragma once
+#include <cstdint>
+
+namespace nqb200 {
+
+constexpr uint32_t kIdleC = 0x80000000u;  // sentinel: free column outside the board
+constexpr uint32_t kIdleL = 0x40000000u;  // ...that the shifted diagonal blocks
+
+struct DfsParams {
+  const uint4* subs;                 // packed records (nq_sub)
+  unsigned long long count;          // records in subs
+  unsigned long long* cursor;        // device dispatch counter (zeroed per launch)
+  unsigned long long* totals;        // [0] weighted, [1] raw sols, [2] iterations,
+                                     // [3] subproblems, [4] first bad record + 1
+  unsigned long long* each_count;    // per-record outputs (PER_SUB only)
+  int* each_high;
+  unsigned long long* each_nodes;
+  uint32_t mask;                     // board_mask(n)
+  int n;
+  int min_placed;                    // batch pre_rows: deeper records would overflow the stack
+  int reverse;                       // dispatch order: 1 = last record first
+  int lastrow;                       // variant (affects high-water / node outputs only)
+};
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
+                                       uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y),
+               "r"(z), "r"(w)
+               : "memory");
+}
+
+__device__ __forceinline__ void lds128(uint32_t addr, uint32_t& x, uint32_t& y, uint32_t& z,
+                                       uint32_t& w) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+               : "r"(addr)
+               : "memory");
+}
+
+// One DFS node for one lane, written in PTX so that the push / descend / stay / pop
+// transitions stay predicated (no select chains) and the arithmetic can use the FMA
+// pipe: p is a valid position, so it is disjoint from l, r and a subset of C and a,
+// which turns |, ^ into +, - (IMAD-able).
+//   p  = a & -a                      lowest untried candidate      (bitboard.hpp:25-28)
+//   a2 = a - p                       candidates left on this row
+//   nC = C - p, nl = (l + p) << 1, nr = (r + p) >> 1               (bitboard.hpp:38-45)
+//   nv = nC & ~(nl | nr)             child's candidates (LOP3 0x10) (bitboard.hpp:21-23)
+//   its += (a != 0)   (bit 31 of -a; a < 2^31)      sol += (nC == 0)
+//   push (C,l,r,a2) if nv && a2; descend if nv; pop if !nv && !a2 && a
+template <uint32_t STRIDE>
+__device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
+                                         uint32_t& sp, uint32_t& sol, uint32_t& its) {
+  asm volatile(
+      "{\n\t"
+      ".reg .u32 na, p, a2, nC, lp, rp, nl, nr, nv, hb;\n\t"
+      ".reg .pred pd, pa, ps, pu, pk, po;\n\t"
+      "neg.s32 na, %3;\n\t"
+      "and.b32 p, %3, na;\n\t"
+      "xor.b32 a2, %3, p;\n\t"
+      "sub.u32 nC, %0, p;\n\t"
+      "add.u32 lp, %1, p;\n\t"
+      "add.u32 rp, %2, p;\n\t"
+      "add.u32 nl, lp, lp;\n\t"
+      "mul.hi.u32 nr, rp, 0x80000000;\n\t"
+      "lop3.b32 nv, nC, nl, nr, 0x10;\n\t"
+      "mad.hi.u32 %6, na, 2, %6;\n\t"
+      "setp.eq.u32 ps, nC, 0;\n\t"
+      "@ps add.u32 %5, %5, 1;\n\t"
+      "setp.ne.u32 pd, nv, 0;\n\t"
+      "setp.ne.u32 pa, a2, 0;\n\t"
+      "setp.ne.u32 pk, p, 0;\n\t"
+      "and.pred pu, pd, pa;\n\t"
+      "@pu st.shared.v4.u32 [%4], {%0, %1, %2, a2};\n\t"
+      "@pu add.u32 %4, %4, %7;\n\t"
+      "selp.b32 %3, nv, a2, pd;\n\t"
+      "@pd mov.b32 %0, nC;\n\t"
+      "@pd mov.b32 %1, nl;\n\t"
+      "@pd mov.b32 %2, nr;\n\t"
+      "or.pred po, pd, pa;\n\t"
+      "and.pred po, !po, pk;\n\t"
+      "@po sub.u32 %4, %4, %7;\n\t"
+      "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t"
+      "}"
+      : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+      : "n"(STRIDE)
+      : "memory");
+}
+
+template <int BLOCK, int KSTEP, bool PER_SUB>
+__global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
+  extern __shared__ uint4 stk[];  // [levels][BLOCK] frames
+  constexpr uint32_t STRIDE = BLOCK * 16u;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t base0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) + threadIdx.x * 16u;
+  const uint32_t base1 = base0 + STRIDE;  // first real frame (level 1)
+
+  // Level 0 holds the idle sentinel that an exhausted lane pops into.
+  sts128(base0, kIdleC, kIdleL, 0u, 0u);
+
+  uint32_t C = kIdleC, l = kIdleL, r = 0u, a = 0u;  // current row state (idle)
+  uint32_t sp = base1;                             // next free frame
+  uint32_t sol = 0u, its = 0u;                     // per-lane counters since last fold
+  uint32_t weight = 0u;                            // multiplier of the current record
+  bool busy = false;                               // lane holds a record
+  unsigned long long tot_w = 0ull, tot_raw = 0ull, tot_it = 0ull, tot_subs = 0ull;
+  // PER_SUB bookkeeping
+  unsigned long long cur_idx = 0ull, sub_sol = 0ull, sub_it = 0ull;
+  int placed = 0, high = 0;
+
+  bool exhausted = false;  // warp-uniform: the dispatch cursor ran past count
+  uint32_t blocks = 0u;
+
+  for (;;) {
+    // ---- refill idle lanes (once per KSTEP block) ----------------------------------
+    uint32_t idle = __ballot_sync(0xffffffffu, a == 0u);
+    if (idle) {
+      for (;;) {
+        if (a == 0u && busy) {  // fold the finished record
+          tot_w += static_cast<unsigned long long>(weight) * sol;
+          tot_raw += sol;
+          tot_it += its;
+          tot_subs += 1ull;
+          if constexpr (PER_SUB) {
+            sub_sol += sol;
+            sub_it += its;
+            P.each_count[cur_idx] = sub_sol;
+            P.each_high[cur_idx] = high;
+            P.each_nodes[cur_idx] = P.lastrow ? (sub_it - sub_sol) : sub_it;
+          }
+          sol = 0u;
+          its = 0u;
+          busy = false;
+        }
+        if (exhausted) break;
+        const uint32_t need = __ballot_sync(0xffffffffu, a == 0u);
+        if (need == 0u) break;
+        const uint32_t leader = __ffs(need) - 1u;
+        const uint32_t n_need = __popc(need);
+        unsigned long long first = 0ull;
+        if (lane == leader) first = atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+        first = __shfl_sync(0xffffffffu, first, leader);
+        if (first + n_need >= P.count) exhausted = true;
+        if (a == 0u) {
+          const unsigned long long pos = first + __popc(need & ((1u << lane) - 1u));
+          if (pos < P.count) {
+            const unsigned long long idx = P.reverse ? (P.count - 1ull - pos) : pos;
+            const uint4 s = __ldg(&P.subs[idx]);
+            busy = true;
+            weight = s.w >> 8;
+            placed = static_cast<int>(s.w & 0xffu);
+            if constexpr (PER_SUB) {
+              cur_idx = idx;
+              sub_sol = 0ull;
+              sub_it = 0ull;
+              high = 0;
+            }
+            // Record validation: cols inside the board, one queen per placed row.
+            if ((s.x & ~P.mask) != 0u || __popc(s.x) != placed || placed < P.min_placed) {
+              atomicCAS(P.totals + 4, 0ull, idx + 1ull);
+              weight = 0u;
+            } else if ((s.x | 0u) == P.mask) {
+              sol = 1u;  // fully placed record: cur == last (solver.hpp:246, :305)
+            } else {
+              C = P.mask & ~s.x;
+              l = s.y;
+              r = s.z;
+              a = C & ~(l | r);  // valid_positions (bitboard.hpp:21-23)
+              sp = base1;
+            }
+            if (a == 0u) {  // settled at the root: back to the idle sentinel state
+              C = kIdleC;
+              l = kIdleL;
+              r = 0u;
+            }
+          }
+        }
+      }
+      if (exhausted && __all_sync(0xffffffffu, a == 0u)) break;
+    }
+
+    // ---- KSTEP predicated DFS steps -------------------------------------------------
+#pragma unroll
+    for (int k = 0; k < KSTEP; ++k) {
+      if constexpr (PER_SUB) {
+        const int row = P.n - __popc(C & P.mask);
+        const int h = row - placed + 1;
+        if (a != 0u && (!P.lastrow || row <= P.n - 2) && h > high) high = h;
+      }
+      dfs_step<STRIDE>(C, l, r, a, sp, sol, its);
+    }
+
+    // Fold u32 counters periodically so they cannot wrap (≤ 2^16*KSTEP steps).
+    if (((++blocks) & 0xffffu) == 0u) {
+      tot_w += static_cast<unsigned long long>(weight) * sol;
+      tot_raw += sol;
+      tot_it += its;
+      if constexpr (PER_SUB) {
+        sub_sol += sol;
+        sub_it += its;
+      }
+      sol = 0u;
+      its = 0u;
+    }
+  }
+
+  // ---- warp reduction, one atomic per warp per total --------------------------------
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    tot_w += __shfl_down_sync(0xffffffffu, tot_w, off);
+    tot_raw += __shfl_down_sync(0xffffffffu, tot_raw, off);
+    tot_it += __shfl_down_sync(0xffffffffu, tot_it, off);
+    tot_subs += __shfl_down_sync(0xffffffffu, tot_subs, off);
+  }
+  if (lane == 0u) {
+    atomicAdd(P.totals + 0, tot_w);
+    atomicAdd(P.totals + 1, tot_raw);
+    atomicAdd(P.totals + 2, tot_it);
+    atomicAdd(P.totals + 3, tot_subs);
+  }
+}
+
+}  // namespace nqb200

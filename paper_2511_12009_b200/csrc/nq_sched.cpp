@@ -1,0 +1,338 @@
+// nq_sched.cpp — the multi-GPU chunk scheduler: execute_batch / execute on devices.
+//
+// Reference: execute_batch (scheduler.hpp:446-569) spawns W std::threads, each running
+// count_with over a contiguous range (uniform / weighted) or over chunks taken from an
+// atomic cursor (stealing), with checked multiplier-weighted partial sums, the first
+// failure rethrown after join, and a checked final sum. Here the same W workers each
+// drive one device stream (worker w -> devices[w % G], own pooled context) and hand
+// whole ranges / chunks to the persistent DFS kernel instead of one subproblem at a
+// time. The extra GUIDED strategy is the GPU default: chunks shrink as the stream
+// drains and are taken from the expensive end first, so the devices
+// finish together.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "nq_gpu.h"
+#include "nq_internal.h"
+
+namespace nqb200 {
+namespace {
+
+bool add_ok(uint64_t a, uint64_t b, uint64_t* r) { return !__builtin_add_overflow(a, b, r); }
+
+std::string timestamp() {
+  using namespace std::chrono;
+  const auto now = system_clock::now();
+  const auto ms = duration_cast<milliseconds>(now.time_since_epoch()) % 1000;
+  const std::time_t t = system_clock::to_time_t(now);
+  std::tm tm{};
+  localtime_r(&t, &tm);
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "[%04d-%02d-%02d %02d:%02d:%02d.%03d]", tm.tm_year + 1900,
+                tm.tm_mon + 1, tm.tm_mday, tm.tm_hour, tm.tm_min, tm.tm_sec,
+                static_cast<int>(ms.count()));
+  return buf;
+}
+
+// Pooled contexts keyed by (device, slot): workers sharing a device get separate streams.
+struct Pool {
+  std::mutex mu;
+  std::vector<std::vector<nq_ctx*>> ctx;  // [device][slot]
+};
+Pool& pool() {
+  static Pool* p = new Pool;  // intentionally leaked: contexts live for the process
+  return *p;
+}
+
+int pooled_ctx(int device, int slot, nq_ctx** out) {
+  Pool& p = pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (static_cast<int>(p.ctx.size()) <= device) p.ctx.resize(device + 1);
+  auto& v = p.ctx[device];
+  if (static_cast<int>(v.size()) <= slot) v.resize(slot + 1, nullptr);
+  if (!v[slot])
+    if (int rc = nq_ctx_create(device, &v[slot])) return rc;
+  *out = v[slot];
+  return NQ_OK;
+}
+
+void emit(const nq_solve_opts& o, int kind, int i, uint64_t u, double d) {
+  if (!o.log) return;
+  char buf[256];
+  nq_format_log(kind, i, u, d, buf, sizeof buf);
+  o.log(o.log_user, buf);
+}
+
+}  // namespace
+}  // namespace nqb200
+
+using namespace nqb200;
+
+extern "C" int nq_format_log(int kind, int i, uint64_t u, double d, char* buf, uint64_t cap) {
+  if (!buf || cap == 0) return set_error(NQ_ECONFIG, "null log buffer");
+  char body[200];
+  switch (kind) {  // scheduler.hpp:357-383
+    case NQ_LOG_GENERATION:
+      std::snprintf(body, sizeof body, "Use %.2fms to generate %llu subproblems!", d,
+                    static_cast<unsigned long long>(u));
+      break;
+    case NQ_LOG_START:
+      std::snprintf(body, sizeof body, "worker [%d] start job, with %llu(%.2f) subproblems.", i,
+                    static_cast<unsigned long long>(u), d);
+      break;
+    case NQ_LOG_FINISH:
+      std::snprintf(body, sizeof body, "worker [%d] finish job.", i);
+      break;
+    case NQ_LOG_RESULT:
+      std::snprintf(body, sizeof body, "n %d queens result %llu, calc time: [%.2f ms]", i,
+                    static_cast<unsigned long long>(u), d);
+      break;
+    default:
+      return set_error(NQ_ECONFIG, "unknown log kind " + std::to_string(kind));
+  }
+  std::snprintf(buf, cap, "%s %s", timestamp().c_str(), body);
+  return NQ_OK;
+}
+
+extern "C" int nq_partition_uniform(uint64_t task_count, int worker_count, uint64_t* ranges) {
+  if (worker_count < 1) return set_error(NQ_ECONFIG, "worker_count must be >= 1");
+  const uint64_t w = static_cast<uint64_t>(worker_count);
+  const uint64_t base = task_count / w, extra = task_count % w;
+  uint64_t at = 0;
+  for (uint64_t i = 0; i < w; ++i) {
+    const uint64_t len = base + (i < extra ? 1 : 0);  // remainder to the lowest workers
+    ranges[2 * i] = at;
+    ranges[2 * i + 1] = at + len;
+    at += len;
+  }
+  return NQ_OK;
+}
+
+extern "C" int nq_partition_weighted(uint64_t task_count, const double* weights, int worker_count,
+                                     uint64_t* ranges) {
+  if (worker_count < 1 || !weights)
+    return set_error(NQ_ECONFIG, "weighted partition needs at least one weight");
+  double sum = 0;
+  for (int i = 0; i < worker_count; ++i) {
+    if (!(weights[i] > 0)) return set_error(NQ_ECONFIG, "partition weights must be positive");
+    sum += weights[i];
+  }
+  std::vector<uint64_t> len(worker_count);
+  uint64_t given = 0;
+  for (int i = 0; i < worker_count; ++i) {
+    len[i] = static_cast<uint64_t>(std::floor(static_cast<double>(task_count) * (weights[i] / sum)));
+    given += len[i];
+  }
+  for (int i = 0; given < task_count; i = (i + 1) % worker_count) ++len[i], ++given;
+  uint64_t at = 0;
+  for (int i = 0; i < worker_count; ++i) {
+    ranges[2 * i] = at;
+    ranges[2 * i + 1] = at + len[i];
+    at += len[i];
+  }
+  return NQ_OK;
+}
+
+extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t count,
+                              const nq_solve_opts* opts, nq_report* out) {
+  using clk = std::chrono::steady_clock;
+  if (!out) return set_error(NQ_ECONFIG, "null report");
+  nq_solve_opts o{};
+  o.variant = NQ_VARIANT_LASTROW;
+  o.strategy = NQ_PARTITION_GUIDED;
+  if (opts) o = *opts;
+  if (o.worker_count < 0) return set_error(NQ_ECONFIG, "worker_count must be >= 1");
+  if (o.strategy == NQ_PARTITION_STEALING && o.chunk == 0)
+    return set_error(NQ_ECONFIG, "chunk_size must be >= 1");
+  if (o.strategy < NQ_PARTITION_UNIFORM || o.strategy > NQ_PARTITION_GUIDED)
+    return set_error(NQ_ECONFIG, "unknown partition strategy " + std::to_string(o.strategy));
+  if (int rc = require_feasible(o.stack_depth, o.config_name, n, pre_rows,
+                                o.variant == NQ_VARIANT_LASTROW))
+    return rc;
+  if (n < 1 || n > 31)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 31] on the GPU path, got " +
+                                     std::to_string(n));
+
+  int ndev = 0;
+  if (int rc = nq_device_count(&ndev)) return rc;
+  std::vector<int> devs;
+  if (o.devices && o.n_devices > 0) {
+    devs.assign(o.devices, o.devices + o.n_devices);
+  } else {
+    const int k = o.n_devices > 0 ? std::min(o.n_devices, ndev) : ndev;
+    for (int i = 0; i < k; ++i) devs.push_back(i);
+  }
+  if (devs.empty()) return set_error(NQ_ECUDA, "no CUDA device visible");
+  const int G = static_cast<int>(devs.size());
+  const int W = o.worker_count > 0 ? o.worker_count : G;
+  if (W > NQ_MAX_WORKERS)
+    return set_error(NQ_ECONFIG, "worker_count above " + std::to_string(NQ_MAX_WORKERS));
+
+  std::vector<uint64_t> ranges;
+  if (o.strategy == NQ_PARTITION_UNIFORM || o.strategy == NQ_PARTITION_WEIGHTED) {
+    ranges.resize(2 * W);
+    int rc;
+    if (o.strategy == NQ_PARTITION_UNIFORM || !o.weights) {
+      if (o.strategy == NQ_PARTITION_WEIGHTED) {
+        std::vector<double> eq(W, 1.0 / W);
+        rc = nq_partition_weighted(count, eq.data(), W, ranges.data());
+      } else {
+        rc = nq_partition_uniform(count, W, ranges.data());
+      }
+    } else {
+      rc = nq_partition_weighted(count, o.weights, W, ranges.data());
+    }
+    if (rc) return rc;
+  }
+
+  std::memset(out, 0, sizeof(*out));
+  out->task_count = count;
+  out->worker_count = W;
+
+  // Dynamic dispensers. stealing: fixed chunks in stream order (scheduler.hpp:536-541);
+  // guided: max(remaining / 2W, floor) from the back of the stream.
+  std::atomic<uint64_t> cursor{0};
+  std::mutex guided_mu;
+  uint64_t guided_taken = 0;
+  const uint64_t guided_floor = o.chunk ? o.chunk : std::max<uint64_t>(count / (16ull * W), 4096);
+  auto take = [&](uint64_t* first, uint64_t* len) -> bool {
+    if (o.strategy == NQ_PARTITION_STEALING) {
+      const uint64_t f = cursor.fetch_add(o.chunk, std::memory_order_relaxed);
+      if (f >= count) return false;
+      *first = f;
+      *len = std::min(o.chunk, count - f);
+      return true;
+    }
+    std::lock_guard<std::mutex> lk(guided_mu);
+    if (guided_taken >= count) return false;
+    const uint64_t rem = count - guided_taken;
+    const uint64_t sz = std::min(rem, std::max<uint64_t>(rem / (2ull * W), guided_floor));
+    *first = count - guided_taken - sz;
+    *len = sz;
+    guided_taken += sz;
+    return true;
+  };
+
+  std::atomic<bool> interrupted{false};
+  std::mutex fail_mu;
+  std::string failure;
+  const auto t0 = clk::now();
+  std::vector<std::thread> threads;
+  threads.reserve(W);
+  for (int w = 0; w < W; ++w) {
+    threads.emplace_back([&, w] {
+      nq_worker_stats& st = out->workers[w];
+      st.worker = w;
+      st.device = devs[w % G];
+      const auto s0 = clk::now();
+      uint64_t first = 0, len = 0;
+      nq_ctx* c = nullptr;
+      int rc = pooled_ctx(st.device, w / G, &c);
+      auto run = [&](uint64_t f, uint64_t l) -> int {
+        nq_result r{};
+        int e = nq_count(c, n, pre_rows, o.variant, subs + f, l, &r);
+        if (e) return e;
+        if (!add_ok(st.partial_sum, r.solutions, &st.partial_sum))
+          return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
+        st.processed += l;
+        st.nodes += r.nodes;
+        st.chunks += 1;
+        st.kernel_ms += r.kernel_ms;
+        return NQ_OK;
+      };
+      if (rc == NQ_OK) {
+        if (!ranges.empty()) {
+          first = ranges[2 * w];
+          len = ranges[2 * w + 1] - first;
+          st.assigned = len;
+          emit(o, NQ_LOG_START, w, len, count ? double(len) / double(count) : 0.0);
+          if (o.cancel && *o.cancel) {
+            interrupted.store(true);
+          } else if (len) {
+            rc = run(first, len);
+          }
+        } else {
+          emit(o, NQ_LOG_START, w, 0, 0.0);
+          while (rc == NQ_OK && !interrupted.load()) {
+            if (o.cancel && *o.cancel) {
+              interrupted.store(true);
+              break;
+            }
+            if (!take(&first, &len)) break;
+            rc = run(first, len);
+          }
+        }
+      }
+      st.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - s0).count();
+      if (rc) {
+        std::lock_guard<std::mutex> lk(fail_mu);
+        if (failure.empty()) {
+          const uint64_t bad = c ? ctx_last_bad(c) : ~0ull;
+          std::string where = bad != ~0ull ? "subproblem " + std::to_string(first + bad)
+                                           : "chunk [" + std::to_string(first) + ", " +
+                                                 std::to_string(first + len) + ")";
+          failure = "worker " + std::to_string(w) + " failed on " + where + ": " + nq_last_error();
+        }
+        interrupted.store(true);
+        return;
+      }
+      emit(o, NQ_LOG_FINISH, w, 0, 0.0);
+    });
+  }
+  for (auto& t : threads) t.join();
+  if (!failure.empty()) return set_error(NQ_ECUDA, failure);
+  out->calc_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+  uint64_t total = 0, nodes = 0;
+  for (int w = 0; w < W; ++w) {
+    if (!add_ok(total, out->workers[w].partial_sum, &total))
+      return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
+    nodes += out->workers[w].nodes;
+  }
+  out->total = total;
+  out->nodes = nodes;
+  out->completed = interrupted.load() ? 0 : 1;
+  return NQ_OK;
+}
+
+extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out) {
+  using clk = std::chrono::steady_clock;
+  if (!out) return set_error(NQ_ECONFIG, "null report");
+  nq_solve_opts o{};
+  o.variant = NQ_VARIANT_LASTROW;
+  o.strategy = NQ_PARTITION_GUIDED;
+  if (opts) o = *opts;
+  if (n < 1 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
+  if (n == 1) {  // execute's short-circuit (scheduler.hpp:576-590)
+    std::memset(out, 0, sizeof(*out));
+    out->total = 1;
+    out->completed = 1;
+    out->worker_count = o.worker_count > 0 ? std::min(o.worker_count, NQ_MAX_WORKERS) : 1;
+    for (int w = 0; w < out->worker_count; ++w) out->workers[w].worker = w;
+    out->workers[0].partial_sum = 1;
+    emit(o, NQ_LOG_RESULT, 1, 1, 0.0);
+    return NQ_OK;
+  }
+  const auto g0 = clk::now();
+  uint64_t total = 0;
+  if (int rc = count_subproblems(n, pre_rows, &total)) return rc;
+  std::vector<nq_sub> batch(total);
+  if (int rc = generate_slice(n, pre_rows, 1, 0, batch.data(), total, &total)) return rc;
+  const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
+  emit(o, NQ_LOG_GENERATION, 0, total, gen_ms);
+  const int rc = nq_solve_batch(n, pre_rows, batch.data(), total, &o, out);
+  if (rc) return rc;
+  out->generation_ms = gen_ms;
+  if (out->completed) emit(o, NQ_LOG_RESULT, n, out->total, out->calc_ms);
+  return NQ_OK;
+}

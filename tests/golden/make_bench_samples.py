@@ -1,0 +1,39 @@
+"""Pin the bench's CPU-baseline samples: node count and weighted total of the systematic
+slices (records i ≡ 0 mod stride) of the N=20 frontier, computed with the C oracle
+(multi-threaded) and cross-checked against the reference build's total when present.
+The GPU test tests/test_gpu_parity.py::test_bench_samples re-derives them on the device.
+
+    python tests/golden/make_bench_samples.py
+"""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle_ctypes import Oracle, Reference, reference_available  # noqa: E402
+from paper_2511_12009_b200 import nqueens as nq  # noqa: E402
+
+PLANS = [(20, 6, 256), (20, 6, 128), (18, 6, 16), (16, 5, 1)]
+
+
+def main():
+    o = Oracle()
+    path = os.path.join(HERE, "bench_samples.json")
+    out = json.load(open(path)) if os.path.exists(path) else {}
+    for n, r, stride in PLANS:
+        key = f"{n},{r},{stride}"
+        if key in out:
+            continue
+        s = nq.generate_slice(n, r, stride, 0)
+        total, nodes = o.solve_batch(n, s)
+        if reference_available() and len(s) < 100000:
+            assert Reference().execute_batch(n, r, s, workers=os.cpu_count())[0] == total
+        out[key] = {"records": len(s), "nodes": nodes, "total": total}
+        print(key, out[key], flush=True)
+        json.dump(out, open(path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

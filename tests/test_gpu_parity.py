@@ -1,0 +1,227 @@
+"""GPU parity: the sm_100a DFS kernel through the C ABI vs the reference (golden
+vectors recorded from the reference build), the C oracle, OEIS A000170 and the
+Appendix-B node counts. Bit-exact throughout (integer path).
+
+Mirrors test_solver.cpp, test_scheduler.cpp and acceptance.cpp criteria 1, 3, 4, 7, 9.
+"""
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2511_12009_b200 import _lib
+from paper_2511_12009_b200 import nqueens as nq
+
+pytestmark = pytest.mark.gpu
+
+CFG1 = nq.builtin_configs[0]
+
+
+def as_recs(lst):
+    return np.array([tuple(r) for r in lst], dtype=_lib.SUB_DTYPE)
+
+
+class Ctx:
+    def __init__(self, block=0, bps=0, reverse=1):
+        self.p = ctypes.c_void_p()
+        _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(self.p)))
+        _lib.check(_lib.lib.nq_ctx_set_tuning(self.p, block, bps, reverse))
+
+    def count(self, n, pre_rows, a, variant=_lib.VARIANT_LASTROW):
+        r = _lib.NqResult()
+        _lib.check(_lib.lib.nq_count(self.p, n, pre_rows, variant, a.ctypes.data if len(a) else None,
+                                     len(a), ctypes.byref(r)))
+        return r
+
+    def close(self):
+        _lib.lib.nq_ctx_destroy(self.p)
+
+
+def test_per_subproblem_vs_reference_golden(golden):
+    """Every subproblem n<=12, R in {1,2,3}: count + high_water, iterative and lastrow
+    (test_solver.cpp:70-80, :92-103, :116-134; acceptance criterion 3)."""
+    for key, d in golden["per_subproblem"].items():
+        n, r = map(int, key.split(","))
+        a = as_recs(d["records"])
+        for variant, ref in (("iterative", d["iterative"]), ("lastrow", d["lastrow"])):
+            c, h, _ = nq.count_each(n, a, nq.KernelVariant[variant], pre_rows=r)
+            assert c.tolist() == [x[0] for x in ref], (key, variant)
+            assert h.tolist() == [x[1] for x in ref], (key, variant)
+        c, _, _ = nq.count_each(n, a, nq.KernelVariant.iterative, pre_rows=r)
+        assert c.tolist() == d["recursive"]
+
+
+def test_per_subproblem_nodes_vs_oracle(oracle):
+    """Alg. 3 node counts per subproblem equal the oracle's loop iterations."""
+    for n, r in [(10, 3), (12, 4), (14, 5)]:
+        a = oracle.generate(n, r)
+        c, h, nodes = nq.count_each(n, a, nq.KernelVariant.lastrow, pre_rows=r)
+        for i in range(0, len(a), max(1, len(a) // 300)):
+            oc, oh, on = oracle.count_lastrow(n, tuple(int(x) for x in a[i]))
+            assert (int(c[i]), int(h[i]), int(nodes[i])) == (oc, oh, on), (n, r, i)
+
+
+def test_shallow_roots_and_full_boards():
+    # test_solver.cpp:82-90, :105-114
+    sol = [0, 2, 4, 1, 3]
+    cur = left = right = 0
+    for col in sol:
+        s = nq.apply_placement(cur, left, right, 1 << col)
+        cur, left, right = s.cur, s.left, s.right
+    sub = nq.Subproblem(cur, left, right, 5, 1)
+    assert cur == nq.board_mask(5)
+    assert nq.count_iterative(5, sub, CFG1).count == 1
+    assert nq.count_iterative_lastrow(5, sub, CFG1).count == 1
+    assert nq.count_iterative_lastrow(1, nq.Subproblem(), CFG1).count == 1
+    assert nq.count_iterative_lastrow(4, nq.Subproblem(), CFG1).count == 2
+    for n in (1, 2, 3):
+        assert nq.count_recursive(n, nq.Subproblem()) == [1, 0, 0][n - 1]
+
+
+def test_q_of_n_1_to_18(golden):
+    """acceptance criterion 1 / 9 at GPU sizes."""
+    for n in range(1, 19):
+        r = min(6, n - 1) if n > 1 else 1
+        rep = nq.execute(n, r, nq.ExecuteOptions(config=CFG1))
+        assert rep.total == golden["oeis_a000170"][n - 1], n
+        assert rep.completed
+
+
+def test_node_counts_appendix_b(golden):
+    """Device node counter == Appendix B (exact, reference generator) for N=14..18."""
+    for n in range(14, 19):
+        for r, nodes in golden["appendix_b_nodes"][str(n)].items():
+            rep = nq.execute(n, int(r), nq.ExecuteOptions(config=CFG1))
+            assert rep.total == golden["oeis_a000170"][n - 1]
+            assert rep.nodes == nodes, (n, r)
+
+
+@pytest.mark.slow
+def test_n20_full(golden):
+    rep = nq.execute(20, 6, nq.ExecuteOptions(config=CFG1))
+    assert rep.total == 39029188884
+    assert rep.nodes == golden["appendix_b_nodes"]["20"]["6"]
+
+
+def test_totals_invariant_across_strategies_and_workers():
+    """test_scheduler.cpp:77-111: exactly-once processing, partial sums add up."""
+    expected = nq.execute(12, 2, nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 1))).total
+    assert expected == 14200
+    for strategy in nq.PartitionStrategy:
+        for workers in (1, 2, 4, 8):
+            plan = nq.PartitionPlan(strategy, workers, [], 3)
+            if strategy is nq.PartitionStrategy.weighted and workers == 8:
+                plan.weights = list(nq.paper_gpu_weights)
+            rep = nq.execute(12, 2, nq.ExecuteOptions(plan=plan))
+            assert rep.total == expected and rep.completed
+            assert sum(w.processed for w in rep.workers) == rep.task_count
+            assert sum(w.partial_sum for w in rep.workers) == rep.total
+            if strategy in (nq.PartitionStrategy.uniform, nq.PartitionStrategy.weighted):
+                assert sum(w.assigned for w in rep.workers) == rep.task_count
+
+
+def test_kernel_flag_same_totals():
+    # test_scheduler.cpp:113-119
+    a = nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 2))
+    b = nq.ExecuteOptions(kernel=nq.KernelVariant.iterative,
+                          plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 2))
+    assert nq.execute(11, 3, a).total == nq.execute(11, 3, b).total == 2680
+
+
+def test_n1_short_circuit():
+    rep = nq.execute(1, 1, nq.ExecuteOptions())
+    assert rep.total == 1 and rep.workers[0].partial_sum == 1
+
+
+def test_log_lines_emitted():
+    lines = []
+    rep = nq.execute(10, 3, nq.ExecuteOptions(log=lines.append,
+                                              plan=nq.PartitionPlan(nq.PartitionStrategy.stealing, 2, [], 16)))
+    assert rep.total == 724
+    assert any("generate" in l for l in lines)
+    assert sum("start job" in l for l in lines) == 2 and sum("finish job" in l for l in lines) == 2
+    assert "n 10 queens result 724, calc time:" in lines[-1]
+
+
+def test_cancel_before_start():
+    ev = threading.Event()
+    ev.set()
+    rep = nq.execute(12, 3, nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.stealing, 2, [], 8)))
+    assert not rep.completed
+
+
+def test_tuning_variants_identical(oracle):
+    a = oracle.generate(15, 5)
+    base = None
+    for block in (64, 96, 128, 192, 256):
+        for reverse in (0, 1):
+            for bps in (0, 1):
+                c = Ctx(block, bps, reverse)
+                r = c.count(15, 5, a)
+                c.close()
+                got = (r.solutions, r.raw_solutions, r.nodes, r.subproblems)
+                base = base or got
+                assert got == base, (block, reverse, bps)
+    assert base[0] == 2279184 and base[3] == len(a)
+
+
+def test_random_subsets_and_permutations(oracle):
+    """Order and batch composition never change a per-record result."""
+    rng = np.random.default_rng(2511)
+    a = oracle.generate(14, 4)
+    ref_counts = oracle.solve_batch(14, a, per_sub=True)[2]
+    for _ in range(4):
+        idx = rng.permutation(len(a))[: rng.integers(1, len(a))]
+        c, _, _ = nq.count_each(14, a[idx], nq.KernelVariant.lastrow, pre_rows=4)
+        assert np.array_equal(c, ref_counts[idx])
+
+
+def test_mixed_depth_batch(oracle):
+    """Records of different placed_rows in one launch (stack sized by the minimum)."""
+    parts = [oracle.generate(13, r) for r in (2, 3, 4)]
+    a = np.concatenate(parts)
+    ctx = Ctx()
+    r = ctx.count(13, 2, a)
+    ctx.close()
+    assert r.solutions == 3 * 73712
+
+
+def test_empty_and_rejected_batches():
+    ctx = Ctx()
+    r = ctx.count(10, 3, np.zeros(0, dtype=_lib.SUB_DTYPE))
+    assert r.solutions == 0 and r.subproblems == 0
+    bad = nq.generate_packed(10, 3)
+    bad[5]["cols"] |= 1 << 12  # outside the board
+    with pytest.raises(_lib.NqError) as e:
+        ctx.count(10, 3, bad)
+    assert e.value.code == _lib.NQ_ECONFIG and "record 5" in str(e.value)
+    shallow = nq.generate_packed(10, 2)
+    with pytest.raises(_lib.NqError):
+        ctx.count(10, 3, shallow)  # placed_rows below the declared pre_rows
+    ctx.close()
+    opts = nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 2))
+    with pytest.raises(RuntimeError) as e:
+        nq.execute_batch(10, 3, bad, opts)
+    assert "failed on subproblem 5" in str(e.value)
+
+
+def test_device_resident_async_path(oracle):
+    import torch
+    a = oracle.generate(16, 5)
+    d = torch.from_numpy(a.view(np.uint32).reshape(-1, 4).astype(np.int32)).cuda()
+    ctx = Ctx()
+    _lib.check(_lib.lib.nq_count_device_async(ctx.p, 16, 5, 1, ctypes.c_void_p(d.data_ptr()), len(a)))
+    r = _lib.NqResult()
+    _lib.check(_lib.lib.nq_collect(ctx.p, ctypes.byref(r)))
+    assert r.solutions == 14772512
+    r2 = _lib.NqResult()
+    _lib.check(_lib.lib.nq_count_device(ctx.p, 16, 5, 1, ctypes.c_void_p(d.data_ptr()), len(a),
+                                        ctypes.byref(r2)))
+    assert (r2.solutions, r2.nodes) == (r.solutions, r.nodes) == (14772512, 563126914)
+    ctx.close()
+
+
+def test_int_peak_measurement():
+    ops, mhz = nq.measure_int_peak(0)
+    assert 5e12 < ops < 1e14 and 500 < mhz < 2500
