@@ -4,9 +4,9 @@
  * The reference (/root/reference/proj/include/nqueens/) is a header-only C++ library
  * with no FFI. Its hot path is
  *
- *   execute(n, R, opts)               scheduler.hpp:573   generate + execute_batch
- *   execute_batch(n, R, batch, opts)  scheduler.hpp:446   worker pool over count_with
- *   count_with(variant, n, sub, cfg)  solver.hpp:350      one subproblem, CPU DFS
+ *   execute(n, R, opts)               scheduler.hpp:393   generate + execute_batch
+ *   execute_batch(n, R, batch, opts)  scheduler.hpp:266   worker pool over count_with
+ *   count_with(variant, n, sub, cfg)  solver.hpp:193      one subproblem, CPU DFS
  *   for_each_subproblem / generate    subproblems.hpp:80  folded frontier
  *   count_subproblems                 subproblems.hpp:118
  *
@@ -82,7 +82,7 @@ void nq_ctx_destroy(nq_ctx* ctx);
 int nq_ctx_set_tuning(nq_ctx* ctx, int block, int blocks_per_sm, int reverse_order);
 
 /* Count a batch held in HOST memory (caller-owned, pageable or pinned). Synchronous.
- * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:499-506).
+ * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:319-326).
  * pre_rows is the batch's pre-placement depth R: it sizes the shared-memory stack
  * (n-1-R frames, the Alg. 3 depth of stack_config.hpp:43-45); a record with fewer
  * placed rows than R, cols outside the board, or popcount(cols) != placed_rows is
@@ -100,7 +100,7 @@ int nq_collect(nq_ctx* ctx, nq_result* out);
 
 /* Per-subproblem results (unweighted counts, high-water marks as in
  * KernelResult, solver.hpp:34-41, and Alg. 3 node counts). Host buffers. This is the
- * count_with seam (solver.hpp:350) batched onto the device. */
+ * count_with seam (solver.hpp:193) batched onto the device. */
 int nq_count_each(nq_ctx* ctx, int n, int pre_rows, int variant, const nq_sub* host_subs,
                   uint64_t count, uint64_t* counts, int32_t* high_water, uint64_t* nodes);
 
@@ -113,13 +113,13 @@ int nq_generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_
 /* subproblems.hpp:118-145 */
 int nq_count_subproblems(int n, int pre_rows, uint64_t* total);
 
-/* --- partitions (scheduler.hpp:241-282) ----------------------------------------------- */
+/* --- partitions (scheduler.hpp:61-102) ----------------------------------------------- */
 /* ranges receives worker_count (first, last) pairs. */
 int nq_partition_uniform(uint64_t task_count, int worker_count, uint64_t* ranges);
 int nq_partition_weighted(uint64_t task_count, const double* weights, int worker_count,
                           uint64_t* ranges);
 
-/* --- multi-GPU execution (scheduler.hpp:446 / :573) -------------------------------- */
+/* --- multi-GPU execution (scheduler.hpp:266 / :573) -------------------------------- */
 #define NQ_PARTITION_UNIFORM 0  /* PartitionStrategy::uniform  (scheduler.hpp:26)        */
 #define NQ_PARTITION_WEIGHTED 1 /* PartitionStrategy::weighted                          */
 #define NQ_PARTITION_STEALING 2 /* PartitionStrategy::stealing: fixed chunks, cursor    */

@@ -43,13 +43,13 @@ static void place(uint32_t* cur, uint32_t* left, uint32_t* right, uint32_t p) {
   *right = (*right | p) >> 1;
 }
 
-/* detail::check_board — solver.hpp:202-205 */
+/* detail::check_board — solver.hpp:45-48 */
 static int check_board(int n) {
   if (n < 1 || n > 32) return fail(NQO_ECONFIG, "board size must be in [1, 32], got %d", n);
   return NQO_OK;
 }
 
-/* count_recursive_impl — solver.hpp:207-220 */
+/* count_recursive_impl — solver.hpp:50-63 */
 static int rec(int n, uint32_t cur, uint32_t left, uint32_t right, uint64_t* out) {
   if (cur == nqo_board_mask(n)) { *out = 1; return NQO_OK; }
   uint64_t sum = 0;
@@ -92,7 +92,7 @@ static int feasible(int stack_depth, int n, int placed, int last_row) {
               "no built-in config is deep enough", stack_depth, n, placed, need);
 }
 
-/* count_iterative — solver.hpp:236-287 */
+/* count_iterative — solver.hpp:79-130 */
 int nqo_count_iterative(int n, const nqo_sub* sub, int stack_depth, uint64_t* count,
                         int* high_water) {
   int rc = check_board(n);
@@ -135,7 +135,7 @@ int nqo_count_iterative(int n, const nqo_sub* sub, int stack_depth, uint64_t* co
   return NQO_OK;
 }
 
-/* count_iterative_lastrow — solver.hpp:295-348. nodes counts loop iterations. */
+/* count_iterative_lastrow — solver.hpp:138-191. nodes counts loop iterations. */
 int nqo_count_lastrow(int n, const nqo_sub* sub, int stack_depth, uint64_t* count,
                       int* high_water, uint64_t* nodes) {
   int rc = check_board(n);
@@ -355,7 +355,7 @@ int nqo_aggregate(const nqo_sub* subs, const uint64_t* counts, uint64_t len, uin
   return rc;
 }
 
-/* partition_uniform — scheduler.hpp:241-253 */
+/* partition_uniform — scheduler.hpp:61-73 */
 int nqo_partition_uniform(uint64_t task_count, int workers, uint64_t* ranges) {
   if (workers < 1) return fail(NQO_ECONFIG, "worker_count must be >= 1");
   const uint64_t base = task_count / (uint64_t)workers, rem = task_count % (uint64_t)workers;
@@ -369,7 +369,7 @@ int nqo_partition_uniform(uint64_t task_count, int workers, uint64_t* ranges) {
   return NQO_OK;
 }
 
-/* partition_weighted — scheduler.hpp:256-282 */
+/* partition_weighted — scheduler.hpp:76-102 */
 int nqo_partition_weighted(uint64_t task_count, const double* weights, int workers,
                            uint64_t* ranges) {
   if (workers < 1) return fail(NQO_ECONFIG, "weighted partition needs at least one weight");
@@ -398,7 +398,7 @@ int nqo_partition_weighted(uint64_t task_count, const double* weights, int worke
   return NQO_OK;
 }
 
-/* ---- threaded batch solve: execute_batch stealing branch, scheduler.hpp:446-569 ---- */
+/* ---- threaded batch solve: execute_batch stealing branch, scheduler.hpp:266-389 ---- */
 
 typedef struct {
   int n;

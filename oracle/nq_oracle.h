@@ -40,12 +40,12 @@ typedef struct {
 uint32_t nqo_board_mask(int n);
 uint32_t nqo_valid_positions(uint32_t cur, uint32_t left, uint32_t right, int n);
 
-/* solver.hpp:207-229 — Alg. 1, plain recursion; multiplier not applied. */
+/* solver.hpp:50-72 — Alg. 1, plain recursion; multiplier not applied. */
 int nqo_count_recursive(int n, uint32_t cur, uint32_t left, uint32_t right, uint64_t* count);
-/* solver.hpp:236-287 — Alg. 2; stack_depth = StackConfig::max_depth() of the config. */
+/* solver.hpp:79-130 — Alg. 2; stack_depth = StackConfig::max_depth() of the config. */
 int nqo_count_iterative(int n, const nqo_sub* sub, int stack_depth, uint64_t* count,
                         int* high_water);
-/* solver.hpp:295-348 — Alg. 3 (last row by popcount). nodes = loop iterations,
+/* solver.hpp:138-191 — Alg. 3 (last row by popcount). nodes = loop iterations,
  * the DFS-node unit of the metric. */
 int nqo_count_lastrow(int n, const nqo_sub* sub, int stack_depth, uint64_t* count,
                       int* high_water, uint64_t* nodes);
@@ -60,13 +60,13 @@ int nqo_aggregate(const nqo_sub* subs, const uint64_t* counts, uint64_t len, uin
 /* subproblems.hpp:169-178 — text export, one line per subproblem. */
 int nqo_write_batch(int n, int pre_rows, FILE* out, uint64_t* lines);
 
-/* scheduler.hpp:241-282 — contiguous partitions. ranges = 2*workers u64 (first,last). */
+/* scheduler.hpp:61-102 — contiguous partitions. ranges = 2*workers u64 (first,last). */
 int nqo_partition_uniform(uint64_t task_count, int workers, uint64_t* ranges);
 int nqo_partition_weighted(uint64_t task_count, const double* weights, int workers,
                            uint64_t* ranges);
 
-/* scheduler.hpp:446-569 restated as a pthread pool with the stealing cursor
- * (scheduler.hpp:536-541): lastrow kernel per subproblem, multiplier-weighted checked
+/* scheduler.hpp:266-389 restated as a pthread pool with the stealing cursor
+ * (scheduler.hpp:356-361): lastrow kernel per subproblem, multiplier-weighted checked
  * sum. Used as the CPU baseline ("port") and to pin node counts. */
 int nqo_solve_batch(int n, const nqo_sub* subs, uint64_t len, int threads, uint64_t chunk,
                     uint64_t* total, uint64_t* nodes, uint64_t* per_sub_counts);

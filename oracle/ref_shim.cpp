@@ -5,7 +5,7 @@
 // Nothing from the reference is copied here: this file only includes the headers and
 // forwards calls, so the oracle restatement (nq_oracle.c) and the CUDA path can be
 // checked against the reference's own code, and so bench.py --impl reference can time
-// the reference's own execute_batch (scheduler.hpp:446) on the GPU box's host cores.
+// the reference's own execute_batch (scheduler.hpp:266) on the GPU box's host cores.
 // Built into oracle/_ref/libnqref.so (git-ignored; travels to the GPU box prebuilt).
 #include <cstdint>
 #include <cstring>
@@ -124,9 +124,9 @@ int nqref_partition(int strategy, uint64_t task_count, int workers, const double
   });
 }
 
-// The reference execute_batch (scheduler.hpp:446-569) on a packed batch. Unpacking
+// The reference execute_batch (scheduler.hpp:266-389) on a packed batch. Unpacking
 // into std::vector<Subproblem> happens before the call and is not part of calc_ms,
-// which is the reference's own steady_clock measurement (scheduler.hpp:486, :562).
+// which is the reference's own steady_clock measurement (scheduler.hpp:306, :382).
 int nqref_execute_batch(int n, int pre_rows, const Packed* subs, uint64_t len, int strategy,
                         int workers, uint64_t chunk, int variant, int config_index,
                         uint64_t* total, double* calc_ms, uint64_t* processed) {
@@ -149,7 +149,7 @@ int nqref_execute_batch(int n, int pre_rows, const Packed* subs, uint64_t len, i
   });
 }
 
-// The reference execute (scheduler.hpp:573-603): generate + execute_batch.
+// The reference execute (scheduler.hpp:393-423): generate + execute_batch.
 int nqref_execute(int n, int pre_rows, int strategy, int workers, uint64_t chunk, int variant,
                   int config_index, uint64_t* total, double* calc_ms, double* gen_ms,
                   uint64_t* task_count) {

@@ -3,11 +3,11 @@
 //
 // Reference counterparts:
 //   nq_count / nq_count_device   the per-worker loop of execute_batch
-//                                (scheduler.hpp:499-506, :521-541) for one device
-//   nq_count_each                count_with per subproblem (solver.hpp:350-354)
-//   nq_solve_batch               execute_batch (scheduler.hpp:446-569): one host thread
+//                                (scheduler.hpp:319-326, :341-362) for one device
+//   nq_count_each                count_with per subproblem (solver.hpp:193-197)
+//   nq_solve_batch               execute_batch (scheduler.hpp:266-389): one host thread
 //                                per GPU, atomic chunk cursor, checked partial sums
-//   nq_solve                     execute (scheduler.hpp:573-603)
+//   nq_solve                     execute (scheduler.hpp:393-423)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -69,7 +69,7 @@ int require_feasible(int stack_depth, const char* config_name, int n, int pre_ro
 // ---- kernel registry ------------------------------------------------------------------
 namespace {
 
-constexpr int kStep = 8;
+constexpr int kStep = 32;  // DFS steps between idle checks (dfs_lab: 32 >= 8 by 3-4%)
 using KernelFn = void (*)(DfsParams);
 
 template <int B>
@@ -381,27 +381,38 @@ int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* hos
 // ---- integer-pipe peak (roofline denominator) -------------------------------------------
 namespace nqb200 {
 
+// LOP3 (ALU pipe) and IMAD (FMA pipe) interleaved 1:1 over CH independent chains per
+// thread, UNR chain steps per loop trip with distinct operands per step (so ptxas can
+// neither fold LOP3 chains nor strength-reduce the IMADs), 2048 threads per SM: the
+// highest thread-level int32 issue rate the SM sustains (both pipes busy).
+constexpr int kPeakCh = 8, kPeakUnr = 8, kPeakIters = 512;
+
 __global__ void __launch_bounds__(512) int_peak_kernel(uint32_t* sink, uint32_t seed,
                                                        unsigned long long* clk) {
-  constexpr int CH = 8, IT = 4096;
-  uint32_t x[CH];
+  uint32_t x[kPeakCh], yy[kPeakUnr], zz[kPeakUnr];
 #pragma unroll
-  for (int i = 0; i < CH; ++i) x[i] = seed ^ (threadIdx.x * 2654435761u + i);
-  const uint32_t y = seed * 7u + 3u, z = seed * 13u + 5u;
+  for (int i = 0; i < kPeakCh; ++i) x[i] = seed ^ (threadIdx.x * 2654435761u + i);
+#pragma unroll
+  for (int u = 0; u < kPeakUnr; ++u) {
+    yy[u] = seed * (7u + 2u * u) + 3u;
+    zz[u] = seed * (13u + 4u * u) + 5u;
+  }
   unsigned long long c0 = 0, t0 = 0;
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     c0 = clock64();
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   }
 #pragma unroll 1
-  for (int it = 0; it < IT; ++it) {
+  for (int it = 0; it < kPeakIters; ++it) {
 #pragma unroll
-    for (int i = 0; i < CH; ++i) {
-      if (i & 1)
-        asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(y), "r"(z));
-      else
-        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
-    }
+    for (int u = 0; u < kPeakUnr; ++u)
+#pragma unroll
+      for (int i = 0; i < kPeakCh; ++i) {
+        if (i & 1)
+          asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(yy[u]), "r"(zz[u]));
+        else
+          asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(yy[u]), "r"(zz[u]));
+      }
   }
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     unsigned long long t1;
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(512) int_peak_kernel(uint32_t* sink, uint32_t 
   }
   uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < CH; ++i) acc ^= x[i];
+  for (int i = 0; i < kPeakCh; ++i) acc ^= x[i];
   if (acc == 0x9e3779b9u) sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
@@ -448,7 +459,7 @@ extern "C" int nq_measure_int_peak(int device, double* ops_per_s, double* sm_mhz
   cudaFree(sink);
   cudaFree(clk);
   NQ_CUDA(cudaGetLastError());
-  const double ops = double(threads) * blocks * 4096.0 * 8.0;
+  const double ops = double(threads) * blocks * kPeakIters * kPeakCh * kPeakUnr;
   *ops_per_s = ops / (best * 1e-3);
   *sm_mhz = hc[1] ? double(hc[0]) / double(hc[1]) * 1e3 : 0.0;
   return NQ_OK;

@@ -1,25 +1,29 @@
 // nq_kernel.cuh — the sm_100a persistent DFS counting kernel.
 //
 // Replaces the reference's per-subproblem CPU search (count_iterative_lastrow,
-// solver.hpp:295-348, called once per subproblem from execute_batch,
-// scheduler.hpp:499-506) with one persistent kernel that owns the whole batch.
+// solver.hpp:138-191, called once per subproblem from execute_batch,
+// scheduler.hpp:319-326) with one persistent kernel that owns the whole batch.
 //
 // Execution model:
 //   * one subproblem per thread; a grid of (#SM x resident blocks) threads stays
 //     resident and refills idle lanes from a global atomic dispatch cursor, one
 //     atomicAdd per warp per refill round (ballot -> leader atomic -> shfl);
 //   * the CURRENT row's state (free columns C, diagonals l/r, untried candidates a)
-//     lives in registers; only rows with untried candidates left are pushed, as one
+//     lives in registers. Each step places the lowest candidate and ALWAYS moves to
+//     the child row; a row that still has untried candidates is pushed first, as one
 //     16-byte frame, onto a per-thread stack in shared memory laid out interleaved
-//     (level L of thread t at frame index L*BLOCK + t), so that every LDS.128/STS.128
-//     quarter-warp touches 32 distinct banks whatever depth each lane is at;
-//   * the loop body is branch-free: push, descend, stay and pop are predicated;
-//     the popcount of Alg. 3's last-row test is replaced by "no free column left"
-//     (the LOP3 zero flag), because POPC issues at 1/4 of the ALU rate on sm_100;
-//   * an exhausted lane pops the level-0 sentinel frame and becomes idle-stable
-//     (a == 0 disables every side effect), so the idle check runs once per K steps;
+//     (level L of thread t at frame index L*BLOCK + t: every quarter-warp of an
+//     LDS.128/STS.128 touches 32 distinct banks whatever depth each lane is at); a
+//     child with no candidate pops the nearest pushed frame. "Always descend" needs no
+//     select between parent and child state: the push/pop predicates come straight out
+//     of the LOP3 zero flags (tools/microbench/dfs_lab.cu measured it 14% faster than
+//     descend-or-stay with four SELs, which left the ALU pipe the bottleneck);
+//   * the popcount of Alg. 3's last-row test is replaced by "no free column left"
+//     (C == 0), because POPC issues at 1/8 of the ALU rate on sm_100;
+//   * an idle lane holds C = 0, a = 0: every side effect is predicated off, so the
+//     idle check runs once per KSTEP steps;
 //   * per-lane u32 counters are folded into u64 totals at subproblem end and every
-//     2^16 K-step blocks, then warp-shuffle reduced with one atomicAdd per warp.
+//     2^15 K-step blocks, then warp-shuffle reduced with one atomicAdd per warp.
 //
 // Node accounting: one loop iteration places one queen at rows placed..n-1. The
 // reference's Alg. 3 settles row n-1 by popcount instead, so its iteration count is
@@ -29,8 +33,7 @@
 
 namespace nqb200 {
 
-constexpr uint32_t kIdleC = 0x80000000u;  // sentinel: free column outside the board
-constexpr uint32_t kIdleL = 0x40000000u;  // ...that the shifted diagonal blocks
+constexpr uint32_t kIdleC = 0u;  // idle lane: no free column, so no child ever has a candidate
 
 struct DfsParams {
   const uint4* subs;                 // packed records (nq_sub)
@@ -63,47 +66,41 @@ __device__ __forceinline__ void lds128(uint32_t addr, uint32_t& x, uint32_t& y, 
                : "memory");
 }
 
-// One DFS node for one lane, written in PTX so that the push / descend / stay / pop
-// transitions stay predicated (no select chains) and the arithmetic can use the FMA
-// pipe: p is a valid position, so it is disjoint from l, r and a subset of C and a,
-// which turns |, ^ into +, - (IMAD-able).
-//   p  = a & -a                      lowest untried candidate      (bitboard.hpp:25-28)
-//   a2 = a - p                       candidates left on this row
-//   nC = C - p, nl = (l + p) << 1, nr = (r + p) >> 1               (bitboard.hpp:38-45)
-//   nv = nC & ~(nl | nr)             child's candidates (LOP3 0x10) (bitboard.hpp:21-23)
-//   its += (a != 0)   (bit 31 of -a; a < 2^31)      sol += (nC == 0)
-//   push (C,l,r,a2) if nv && a2; descend if nv; pop if !nv && !a2 && a
+// One DFS node for one lane, in PTX so the push / pop transitions stay predicated on
+// the zero flags of the LOP3s that produce them. p is a valid position, so it is
+// disjoint from l, r and a subset of C and a, which turns |, ^ into +, - (the FMA
+// pipe can take them):
+//   p  = a & -a                         lowest untried candidate   (bitboard.hpp:25-28)
+//   a  = a ^ p;  push (C,l,r,a) if a    the row's remaining candidates
+//   C -= p, l = (l + p) << 1, r = (r + p) >> 1                     (bitboard.hpp:38-45)
+//   a  = C & ~(l | r)                   child's candidates (LOP3 0x10) (bitboard.hpp:21-23)
+//   its += (a_in != 0)  (bit 31 of -a_in; a_in < 2^31),  sol += (C == 0) for busy lanes
+//   pop (C,l,r,a) if the child has no candidate and the lane is busy
 template <uint32_t STRIDE>
 __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
                                          uint32_t& sp, uint32_t& sol, uint32_t& its) {
   asm volatile(
       "{\n\t"
-      ".reg .u32 na, p, a2, nC, lp, rp, nl, nr, nv, hb;\n\t"
-      ".reg .pred pd, pa, ps, pu, pk, po;\n\t"
+      ".reg .u32 na, p;\n\t"
+      ".reg .pred pa, pk, po, ps;\n\t"
       "neg.s32 na, %3;\n\t"
       "and.b32 p, %3, na;\n\t"
-      "xor.b32 a2, %3, p;\n\t"
-      "sub.u32 nC, %0, p;\n\t"
-      "add.u32 lp, %1, p;\n\t"
-      "add.u32 rp, %2, p;\n\t"
-      "add.u32 nl, lp, lp;\n\t"
-      "mul.hi.u32 nr, rp, 0x80000000;\n\t"
-      "lop3.b32 nv, nC, nl, nr, 0x10;\n\t"
-      "mad.hi.u32 %6, na, 2, %6;\n\t"
-      "setp.eq.u32 ps, nC, 0;\n\t"
-      "@ps add.u32 %5, %5, 1;\n\t"
-      "setp.ne.u32 pd, nv, 0;\n\t"
-      "setp.ne.u32 pa, a2, 0;\n\t"
       "setp.ne.u32 pk, p, 0;\n\t"
-      "and.pred pu, pd, pa;\n\t"
-      "@pu st.shared.v4.u32 [%4], {%0, %1, %2, a2};\n\t"
-      "@pu add.u32 %4, %4, %7;\n\t"
-      "selp.b32 %3, nv, a2, pd;\n\t"
-      "@pd mov.b32 %0, nC;\n\t"
-      "@pd mov.b32 %1, nl;\n\t"
-      "@pd mov.b32 %2, nr;\n\t"
-      "or.pred po, pd, pa;\n\t"
-      "and.pred po, !po, pk;\n\t"
+      "xor.b32 %3, %3, p;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\t"
+      "@pa st.shared.v4.u32 [%4], {%0, %1, %2, %3};\n\t"
+      "@pa add.u32 %4, %4, %7;\n\t"
+      "sub.u32 %0, %0, p;\n\t"
+      "add.u32 %1, %1, p;\n\t"
+      "add.u32 %1, %1, %1;\n\t"
+      "add.u32 %2, %2, p;\n\t"
+      "shr.u32 %2, %2, 1;\n\t"
+      "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"
+      "shr.u32 na, na, 31;\n\t"
+      "add.u32 %6, %6, na;\n\t"
+      "setp.eq.and.u32 ps, %0, 0, pk;\n\t"
+      "@ps add.u32 %5, %5, 1;\n\t"
+      "setp.eq.and.u32 po, %3, 0, pk;\n\t"
       "@po sub.u32 %4, %4, %7;\n\t"
       "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t"
       "}"
@@ -121,9 +118,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   const uint32_t base1 = base0 + STRIDE;  // first real frame (level 1)
 
   // Level 0 holds the idle sentinel that an exhausted lane pops into.
-  sts128(base0, kIdleC, kIdleL, 0u, 0u);
+  sts128(base0, kIdleC, 0u, 0u, 0u);
 
-  uint32_t C = kIdleC, l = kIdleL, r = 0u, a = 0u;  // current row state (idle)
+  uint32_t C = kIdleC, l = 0u, r = 0u, a = 0u;  // current row state (idle)
   uint32_t sp = base1;                             // next free frame
   uint32_t sol = 0u, its = 0u;                     // per-lane counters since last fold
   uint32_t weight = 0u;                            // multiplier of the current record
@@ -185,7 +182,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
               atomicCAS(P.totals + 4, 0ull, idx + 1ull);
               weight = 0u;
             } else if ((s.x | 0u) == P.mask) {
-              sol = 1u;  // fully placed record: cur == last (solver.hpp:246, :305)
+              sol = 1u;  // fully placed record: cur == last (solver.hpp:89, :148)
             } else {
               C = P.mask & ~s.x;
               l = s.y;
@@ -193,11 +190,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
               a = C & ~(l | r);  // valid_positions (bitboard.hpp:21-23)
               sp = base1;
             }
-            if (a == 0u) {  // settled at the root: back to the idle sentinel state
-              C = kIdleC;
-              l = kIdleL;
-              r = 0u;
-            }
+            if (a == 0u) C = kIdleC;  // settled at the root: back to the idle state
           }
         }
       }
@@ -215,8 +208,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
       dfs_step<STRIDE>(C, l, r, a, sp, sol, its);
     }
 
-    // Fold u32 counters periodically so they cannot wrap (≤ 2^16*KSTEP steps).
-    if (((++blocks) & 0xffffu) == 0u) {
+    // Fold u32 counters periodically so they cannot wrap (≤ 2^15*KSTEP steps).
+    if (((++blocks) & 0x7fffu) == 0u) {
       tot_w += static_cast<unsigned long long>(weight) * sol;
       tot_raw += sol;
       tot_it += its;

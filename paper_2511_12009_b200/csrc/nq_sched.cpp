@@ -1,6 +1,6 @@
 // nq_sched.cpp — the multi-GPU chunk scheduler: execute_batch / execute on devices.
 //
-// Reference: execute_batch (scheduler.hpp:446-569) spawns W std::threads, each running
+// Reference: execute_batch (scheduler.hpp:266-389) spawns W std::threads, each running
 // count_with over a contiguous range (uniform / weighted) or over chunks taken from an
 // atomic cursor (stealing), with checked multiplier-weighted partial sums, the first
 // failure rethrown after join, and a checked final sum. Here the same W workers each
@@ -81,7 +81,7 @@ using namespace nqb200;
 extern "C" int nq_format_log(int kind, int i, uint64_t u, double d, char* buf, uint64_t cap) {
   if (!buf || cap == 0) return set_error(NQ_ECONFIG, "null log buffer");
   char body[200];
-  switch (kind) {  // scheduler.hpp:357-383
+  switch (kind) {  // scheduler.hpp:177-203
     case NQ_LOG_GENERATION:
       std::snprintf(body, sizeof body, "Use %.2fms to generate %llu subproblems!", d,
                     static_cast<unsigned long long>(u));
@@ -199,7 +199,7 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
   out->task_count = count;
   out->worker_count = W;
 
-  // Dynamic dispensers. stealing: fixed chunks in stream order (scheduler.hpp:536-541);
+  // Dynamic dispensers. stealing: fixed chunks in stream order (scheduler.hpp:356-361);
   // guided: max(remaining / 2W, floor) from the back of the stream.
   std::atomic<uint64_t> cursor{0};
   std::mutex guided_mu;
@@ -313,7 +313,7 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   if (opts) o = *opts;
   if (n < 1 || n > 32)
     return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
-  if (n == 1) {  // execute's short-circuit (scheduler.hpp:576-590)
+  if (n == 1) {  // execute's short-circuit (scheduler.hpp:396-410)
     std::memset(out, 0, sizeof(*out));
     out->total = 1;
     out->completed = 1;

@@ -224,17 +224,17 @@ def _count_one(variant: KernelVariant, n: int, sub: Subproblem, cfg: StackConfig
 
 
 def count_iterative(n: int, sub: Subproblem, cfg: StackConfig) -> KernelResult:
-    """solver.hpp:236 — Alg. 2 semantics, counted on the GPU."""
+    """solver.hpp:79 — Alg. 2 semantics, counted on the GPU."""
     return _count_one(KernelVariant.iterative, n, sub, cfg)
 
 
 def count_iterative_lastrow(n: int, sub: Subproblem, cfg: StackConfig) -> KernelResult:
-    """solver.hpp:295 — Alg. 3 semantics, counted on the GPU."""
+    """solver.hpp:138 — Alg. 3 semantics, counted on the GPU."""
     return _count_one(KernelVariant.lastrow, n, sub, cfg)
 
 
 def count_recursive(n: int, sub: Subproblem) -> int:
-    """solver.hpp:226 — the count only (multiplier not applied), counted on the GPU."""
+    """solver.hpp:69 — the count only (multiplier not applied), counted on the GPU."""
     _check_board(n)
     counts, _, _ = count_each(n, [sub], KernelVariant.iterative, pre_rows=min(sub.placed_rows, n))
     return int(counts[0])
@@ -443,7 +443,7 @@ def log_result_line(n: int, total: int, calc_ms: float) -> str:
 @dataclass
 class ExecuteOptions:
     kernel: KernelVariant = KernelVariant.lastrow
-    config: StackConfig = builtin_configs[1]  # config2 (scheduler.hpp:428)
+    config: StackConfig = builtin_configs[1]  # config2 (scheduler.hpp:248)
     plan: PartitionPlan = field(default_factory=PartitionPlan)
     log: Optional[Callable[[str], None]] = None
     progress: object = None
@@ -504,7 +504,7 @@ def _report(n: int, pre_rows: int, opts: ExecuteOptions, rep) -> SolveReport:
 
 
 def execute_batch(n: int, pre_rows: int, batch, opts: ExecuteOptions) -> SolveReport:
-    """scheduler.hpp:446 on the GPUs: every record exactly once, totals strategy-invariant."""
+    """scheduler.hpp:266 on the GPUs: every record exactly once, totals strategy-invariant."""
     if opts.plan.worker_count < 1:
         raise ConfigError("worker_count must be >= 1")
     if opts.plan.strategy is PartitionStrategy.stealing and opts.plan.chunk_size == 0:
@@ -521,7 +521,7 @@ def execute_batch(n: int, pre_rows: int, batch, opts: ExecuteOptions) -> SolveRe
 
 
 def execute(n: int, pre_rows: int, opts: ExecuteOptions) -> SolveReport:
-    """scheduler.hpp:573: generate + execute_batch (n == 1 short-circuits to Q(1) = 1)."""
+    """scheduler.hpp:393: generate + execute_batch (n == 1 short-circuits to Q(1) = 1)."""
     _check_board(n)
     keep: list = []
     o = _solve_opts(opts, keep)

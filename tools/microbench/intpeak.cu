@@ -15,7 +15,8 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int CH = 8;        // independent chains per thread
-constexpr int ITERS = 4096;  // loop trips; each trip = CH ops
+constexpr int UNR = 8;       // chain steps per loop trip (amortises the loop branch)
+constexpr int ITERS = 512;   // loop trips; each trip = CH * UNR ops
 
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
@@ -26,13 +27,18 @@ __global__ void __launch_bounds__(512) k_ops(uint32_t* out, uint32_t seed, uint6
   uint32_t x[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) x[i] = seed ^ (threadIdx.x * 2654435761u + i);
-  const uint32_t y = seed * 7u + 3u, z = seed * 13u + 5u;
+  uint32_t yy[UNR], zz[UNR];  // distinct operands per step: no LOP3/IMAD chain folding
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) { yy[u] = seed * (7u + 2u * u) + 3u; zz[u] = seed * (13u + 4u * u) + 5u; }
   uint64_t c0 = 0, t0 = 0;
   if (threadIdx.x == 0 && blockIdx.x == 0) { c0 = clock64(); t0 = gtimer(); }
 #pragma unroll 1
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
     for (int i = 0; i < CH; ++i) {
+      const uint32_t y = yy[u], z = zz[u];
       if (OP == 0) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
       if (OP == 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(y), "r"(z));
       if (OP == 2) {  // 1:1 ALU:FMA mix
@@ -74,7 +80,7 @@ int run(const char* name, int sms) {
     float ms; cudaEventElapsedTime(&ms, a, b);
     if (ms < best) { best = ms; CK(cudaMemcpy(hc, clk, 16, cudaMemcpyDeviceToHost)); }
   }
-  const double ops = double(threads) * blocks * ITERS * CH;
+  const double ops = double(threads) * blocks * ITERS * CH * UNR;
   const double rate = ops / (best * 1e-3);
   const double mhz = hc[1] ? double(hc[0]) / double(hc[1]) * 1e3 : 0.0;
   const double per_sm_clk = rate / (sms * mhz * 1e6);
