@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 from oracle_ctypes import Oracle, Reference, reference_available  # noqa: E402
 from paper_2511_12009_b200 import nqueens as nq  # noqa: E402
 
-PLANS = [(20, 6, 256), (20, 6, 128), (18, 6, 16), (16, 5, 1)]
+PLANS = [(20, 6, 256), (20, 6, 128), (20, 7, 256), (20, 7, 128), (18, 6, 16), (16, 5, 1)]
 
 
 def main():
