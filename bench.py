@@ -41,6 +41,18 @@ OEIS = {16: 14772512, 17: 95815104, 18: 666090624, 19: 4968057848, 20: 390291888
 INT_OPS_PER_NODE = 18  # algorithmic int ops of the minimal last-row body
 
 
+def ncu_traffic(n, pre_rows, world):
+    """DRAM bytes (read + write) per launch of the DFS kernel for this workload, from the
+    committed ncu capture (profiles/ncu_dram.json), or None when not captured."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_dram.json")) as f:
+            d = json.load(f)
+    except OSError:
+        return None
+    e = d.get(f"{n},{pre_rows},{world}")
+    return None if e is None else e["dram_bytes_per_launch"]
+
+
 def load_samples():
     with open(os.path.join(REPO, "tests", "golden", "bench_samples.json")) as f:
         return json.load(f)
@@ -176,7 +188,10 @@ def main():
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.pre_rows is None:
-        args.pre_rows = 6
+        # R=7: 22.8 M finer subtrees keep every lane busy to the end (lane efficiency
+        # 99.7% vs 97.9% at R=6, tools/microbench/dfs_lab.cu) and the shallower stack
+        # fits one more block per SM.
+        args.pre_rows = 7 if args.n >= 19 else 6
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -286,10 +301,14 @@ def main():
                    "block": args.block or 128, "order": "expensive-first" if args.order else "stream"},
         "wall_ms": t_dev_max / args.steps,
         "gpu_launches": args.steps,
-        "roofline": {"bound": "int-issue", "achieved": achieved / 1e12, "peak": ops / 1e12,
-                     "unit": "Tint-op/s", "frac": achieved / ops, "traffic": None,
-                     "peak_source": f"measured live: LOP3+IMAD 1:1 stream, all SMs, {mhz:.0f} MHz",
-                     "ops_per_node": INT_OPS_PER_NODE},
+        "roofline": {"bound": "int", "achieved": achieved / 1e12, "peak": ops / 1e12,
+                     "unit": "Tint-op/s", "frac": achieved / ops,
+                     "traffic": ncu_traffic(args.n, args.pre_rows, world),
+                     "peak_source": f"measured live on this GPU: LOP3+IMAD 1:1 int32 stream, "
+                                    f"all SMs, {mhz:.0f} MHz (nq_measure_int_peak)",
+                     "ops_per_node": INT_OPS_PER_NODE,
+                     "algorithmic": f"{INT_OPS_PER_NODE} int ops per DFS node x "
+                                    f"{nodes_all // args.steps} nodes per launch"},
         "clocks": clk,
     }
     if e2e_ms is not None:

@@ -80,6 +80,13 @@ void nq_ctx_destroy(nq_ctx* ctx);
  * dispatch order (0 = as given, 1 = reversed: the expensive tail of the DFS order
  * first). */
 int nq_ctx_set_tuning(nq_ctx* ctx, int block, int blocks_per_sm, int reverse_order);
+/* Shared-memory stack layout of the DFS kernel:
+ *   NQ_LAYOUT_V4      one 16-byte frame per LDS.128/STS.128 (default, fastest);
+ *   NQ_LAYOUT_PLANES  four 32-bit planes, lane t owns bank t: zero bank conflicts for
+ *                     any set of active lanes, four memory instructions per push/pop. */
+#define NQ_LAYOUT_V4 0
+#define NQ_LAYOUT_PLANES 1
+int nq_ctx_set_layout(nq_ctx* ctx, int layout);
 
 /* Count a batch held in HOST memory (caller-owned, pageable or pinned). Synchronous.
  * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:319-326).

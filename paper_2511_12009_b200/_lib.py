@@ -19,6 +19,8 @@ NQ_ECONFIG = -2
 NQ_EOVERFLOW = -3
 NQ_ECANCEL = -4
 
+LAYOUT_V4, LAYOUT_PLANES = 0, 1
+
 VARIANT_ITERATIVE = 0
 VARIANT_LASTROW = 1
 
@@ -99,6 +101,7 @@ _sigs = {
     "nq_ctx_create": (ctypes.c_int, [ctypes.c_int, _P(ctypes.c_void_p)]),
     "nq_ctx_destroy": (None, [ctypes.c_void_p]),
     "nq_ctx_set_tuning": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "nq_ctx_set_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "nq_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_void_p, _u64, _P(NqResult)]),
     "nq_count_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -73,17 +73,20 @@ constexpr int kStep = 32;  // DFS steps between idle checks (dfs_lab: 32 >= 8 by
 using KernelFn = void (*)(DfsParams);
 
 template <int B>
-KernelFn pick(bool per_sub) {
-  return per_sub ? nq_dfs_kernel<B, kStep, true> : nq_dfs_kernel<B, kStep, false>;
+KernelFn pick(bool per_sub, int layout) {
+  if (layout == NQ_LAYOUT_PLANES)
+    return per_sub ? nq_dfs_kernel<B, kStep, true, kLayoutPlanes>
+                   : nq_dfs_kernel<B, kStep, false, kLayoutPlanes>;
+  return per_sub ? nq_dfs_kernel<B, kStep, true, kLayoutV4> : nq_dfs_kernel<B, kStep, false, kLayoutV4>;
 }
 
-KernelFn kernel_for(int block, bool per_sub) {
+KernelFn kernel_for(int block, bool per_sub, int layout) {
   switch (block) {
-    case 64: return pick<64>(per_sub);
-    case 96: return pick<96>(per_sub);
-    case 128: return pick<128>(per_sub);
-    case 192: return pick<192>(per_sub);
-    case 256: return pick<256>(per_sub);
+    case 64: return pick<64>(per_sub, layout);
+    case 96: return pick<96>(per_sub, layout);
+    case 128: return pick<128>(per_sub, layout);
+    case 192: return pick<192>(per_sub, layout);
+    case 256: return pick<256>(per_sub, layout);
     default: return nullptr;
   }
 }
@@ -105,6 +108,7 @@ struct nq_ctx {
   int block = 128;
   int blocks_per_sm = 0;                   // 0 = occupancy limit
   int reverse = 1;
+  int layout = NQ_LAYOUT_V4;
   // in-flight batch (nq_count_device_async / nq_collect)
   bool pending = false;
   int p_variant = 1;
@@ -128,7 +132,7 @@ struct Launch {
 int plan_launch(nq_ctx* c, int n, int pre_rows, bool per_sub, Launch* L) {
   const int frames = std::max(n - 1 - pre_rows, 0);
   const int levels = frames + 1;  // + the idle sentinel
-  L->fn = kernel_for(c->block, per_sub);
+  L->fn = kernel_for(c->block, per_sub, c->layout);
   if (!L->fn) return set_error(NQ_ECONFIG, "unsupported block size " + std::to_string(c->block));
   L->smem = static_cast<size_t>(levels) * c->block * 16u;
   NQ_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -283,13 +287,21 @@ void nq_ctx_destroy(nq_ctx* c) {
 int nq_ctx_set_tuning(nq_ctx* c, int block, int blocks_per_sm, int reverse_order) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
   if (block != 0) {
-    if (!kernel_for(block, false))
+    if (!kernel_for(block, false, c->layout))
       return set_error(NQ_ECONFIG, "unsupported block size " + std::to_string(block) +
                                        " (64, 96, 128, 192, 256)");
     c->block = block;
   }
   c->blocks_per_sm = std::max(blocks_per_sm, 0);
   c->reverse = reverse_order ? 1 : 0;
+  return NQ_OK;
+}
+
+int nq_ctx_set_layout(nq_ctx* c, int layout) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (layout != NQ_LAYOUT_V4 && layout != NQ_LAYOUT_PLANES)
+    return set_error(NQ_ECONFIG, "unknown stack layout " + std::to_string(layout));
+  c->layout = layout;
   return NQ_OK;
 }
 

@@ -76,10 +76,26 @@ __device__ __forceinline__ void lds128(uint32_t addr, uint32_t& x, uint32_t& y, 
 //   a  = C & ~(l | r)                   child's candidates (LOP3 0x10) (bitboard.hpp:21-23)
 //   its += (a_in != 0)  (bit 31 of -a_in; a_in < 2^31),  sol += (C == 0) for busy lanes
 //   pop (C,l,r,a) if the child has no candidate and the lane is busy
-template <uint32_t STRIDE>
+// Stack layouts (both: one level = BLOCK frames = BLOCK*16 bytes):
+//   kLayoutV4     frame of thread t at level L = one uint4 at stk[L*BLOCK + t]; one
+//                 STS.128 / LDS.128 per push / pop. Fastest. A dense warp access is
+//                 conflict-free (every quarter-warp covers the 32 banks once); a sparse
+//                 predicated LDS.128 whose active lanes fall in different quarter-warps
+//                 costs one wavefront per quarter and ncu books the excess over
+//                 ceil(bytes/128) as "bank conflicts" (tools/microbench/smem_banks.cu) —
+//                 no 16-byte-per-lane layout can avoid that.
+//   kLayoutPlanes word w of the frame in plane w: u32 at ((4L + w)*BLOCK + t); lane t
+//                 owns bank t in every plane, so ANY set of active lanes is one
+//                 wavefront per LDS.32/STS.32 — zero bank conflicts by construction,
+//                 at four memory instructions per push / pop (~5% slower, dfs_lab).
+constexpr int kLayoutV4 = 0;
+constexpr int kLayoutPlanes = 1;
+
+template <uint32_t STRIDE, int LAYOUT>
 __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
                                          uint32_t& sp, uint32_t& sol, uint32_t& its) {
-  asm volatile(
+  if constexpr (LAYOUT == kLayoutV4) {
+    asm volatile(
       "{\n\t"
       ".reg .u32 na, p;\n\t"
       ".reg .pred pa, pk, po, ps;\n\t"
@@ -107,18 +123,61 @@ __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, 
       : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
       : "n"(STRIDE)
       : "memory");
+  } else {
+    asm volatile(
+      "{\n\t"
+      ".reg .u32 na, p;\n\t"
+      ".reg .pred pa, pk, po, ps;\n\t"
+      "neg.s32 na, %3;\n\t"
+      "and.b32 p, %3, na;\n\t"
+      "setp.ne.u32 pk, p, 0;\n\t"
+      "xor.b32 %3, %3, p;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\t"
+      "@pa st.shared.u32 [%4], %0;\n\t"
+      "@pa st.shared.u32 [%4+%8], %1;\n\t"
+      "@pa st.shared.u32 [%4+%9], %2;\n\t"
+      "@pa st.shared.u32 [%4+%10], %3;\n\t"
+      "@pa add.u32 %4, %4, %7;\n\t"
+      "sub.u32 %0, %0, p;\n\t"
+      "add.u32 %1, %1, p;\n\t"
+      "add.u32 %1, %1, %1;\n\t"
+      "add.u32 %2, %2, p;\n\t"
+      "shr.u32 %2, %2, 1;\n\t"
+      "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"
+      "shr.u32 na, na, 31;\n\t"
+      "add.u32 %6, %6, na;\n\t"
+      "setp.eq.and.u32 ps, %0, 0, pk;\n\t"
+      "@ps add.u32 %5, %5, 1;\n\t"
+      "setp.eq.and.u32 po, %3, 0, pk;\n\t"
+      "@po sub.u32 %4, %4, %7;\n\t"
+      "@po ld.shared.u32 %0, [%4];\n\t"
+      "@po ld.shared.u32 %1, [%4+%8];\n\t"
+      "@po ld.shared.u32 %2, [%4+%9];\n\t"
+      "@po ld.shared.u32 %3, [%4+%10];\n\t"
+      "}"
+      : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+      : "n"(STRIDE), "n"(STRIDE / 4), "n"(STRIDE / 2), "n"(3 * STRIDE / 4)
+      : "memory");
+  }
 }
 
-template <int BLOCK, int KSTEP, bool PER_SUB>
+template <int BLOCK, int KSTEP, bool PER_SUB, int LAYOUT>
 __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
-  extern __shared__ uint4 stk[];  // [levels][BLOCK] frames
+  extern __shared__ uint4 stk[];  // [levels][BLOCK] frames (or [levels][4][BLOCK] words)
   constexpr uint32_t STRIDE = BLOCK * 16u;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t base0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) + threadIdx.x * 16u;
+  const uint32_t base0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) +
+                         threadIdx.x * (LAYOUT == kLayoutV4 ? 16u : 4u);
   const uint32_t base1 = base0 + STRIDE;  // first real frame (level 1)
 
-  // Level 0 holds the idle sentinel that an exhausted lane pops into.
-  sts128(base0, kIdleC, 0u, 0u, 0u);
+  // Level 0 holds the idle sentinel that an exhausted lane pops into (all zero).
+  if constexpr (LAYOUT == kLayoutV4) {
+    sts128(base0, kIdleC, 0u, 0u, 0u);
+  } else {
+#pragma unroll
+    for (uint32_t w = 0; w < 4; ++w)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(base0 + w * (STRIDE / 4)), "r"(0u) : "memory");
+  }
 
   uint32_t C = kIdleC, l = 0u, r = 0u, a = 0u;  // current row state (idle)
   uint32_t sp = base1;                             // next free frame
@@ -205,7 +264,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         const int h = row - placed + 1;
         if (a != 0u && (!P.lastrow || row <= P.n - 2) && h > high) high = h;
       }
-      dfs_step<STRIDE>(C, l, r, a, sp, sol, its);
+      dfs_step<STRIDE, LAYOUT>(C, l, r, a, sp, sol, its);
     }
 
     // Fold u32 counters periodically so they cannot wrap (≤ 2^15*KSTEP steps).

@@ -23,9 +23,10 @@ def as_recs(lst):
 
 
 class Ctx:
-    def __init__(self, block=0, bps=0, reverse=1):
+    def __init__(self, block=0, bps=0, reverse=1, layout=_lib.LAYOUT_V4):
         self.p = ctypes.c_void_p()
         _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(self.p)))
+        _lib.check(_lib.lib.nq_ctx_set_layout(self.p, layout))
         _lib.check(_lib.lib.nq_ctx_set_tuning(self.p, block, bps, reverse))
 
     def count(self, n, pre_rows, a, variant=_lib.VARIANT_LASTROW):
@@ -154,16 +155,27 @@ def test_cancel_before_start():
 def test_tuning_variants_identical(oracle):
     a = oracle.generate(15, 5)
     base = None
-    for block in (64, 96, 128, 192, 256):
-        for reverse in (0, 1):
-            for bps in (0, 1):
-                c = Ctx(block, bps, reverse)
-                r = c.count(15, 5, a)
-                c.close()
-                got = (r.solutions, r.raw_solutions, r.nodes, r.subproblems)
-                base = base or got
-                assert got == base, (block, reverse, bps)
+    for layout in (_lib.LAYOUT_V4, _lib.LAYOUT_PLANES):
+        for block in (64, 96, 128, 192, 256):
+            for reverse in (0, 1):
+                for bps in (0, 1):
+                    c = Ctx(block, bps, reverse, layout)
+                    r = c.count(15, 5, a)
+                    c.close()
+                    got = (r.solutions, r.raw_solutions, r.nodes, r.subproblems)
+                    base = base or got
+                    assert got == base, (layout, block, reverse, bps)
     assert base[0] == 2279184 and base[3] == len(a)
+
+
+def test_planes_layout_per_subproblem(oracle):
+    """The zero-bank-conflict plane layout gives the same per-record results."""
+    a = oracle.generate(12, 3)
+    want = nq.count_each(12, a, nq.KernelVariant.lastrow, pre_rows=3)
+    c = Ctx(layout=_lib.LAYOUT_PLANES)
+    r = c.count(12, 3, a)
+    c.close()
+    assert r.solutions == 14200 and r.nodes == int(want[2].sum())
 
 
 def test_random_subsets_and_permutations(oracle):

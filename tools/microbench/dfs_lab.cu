@@ -28,6 +28,8 @@ int set_error(int code, const std::string& msg) {
 
 using namespace nqb200;
 
+constexpr uint32_t kIdleL = 0x40000000u;  // lab-only: diagonal mask of the idle sentinel
+
 #define CK(x)                                                                        \
   do {                                                                               \
     cudaError_t e = (x);                                                             \
@@ -159,6 +161,49 @@ __device__ __forceinline__ void ad_step(uint32_t& C, uint32_t& l, uint32_t& r, u
       : "memory");
 }
 
+// Variant AD32: same step, frame split into four 32-bit planes (plane w of level L of
+// thread t at word (4L + w)*BLOCK + t): every lane owns one bank in every plane, so any
+// set of active lanes is one wavefront per LDS.32/STS.32 (zero bank conflicts).
+template <uint32_t STRIDE>
+__device__ __forceinline__ void ad32_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
+                                          uint32_t& sp, uint32_t& sol, uint32_t& its) {
+  constexpr uint32_t P = STRIDE / 4;  // bytes between planes
+  asm volatile(
+      "{\n\t"
+      ".reg .u32 na, p;\n\t"
+      ".reg .pred pa, pk, po, ps;\n\t"
+      "neg.s32 na, %3;\n\t"
+      "and.b32 p, %3, na;\n\t"
+      "setp.ne.u32 pk, p, 0;\n\t"
+      "xor.b32 %3, %3, p;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\t"
+      "@pa st.shared.u32 [%4], %0;\n\t"
+      "@pa st.shared.u32 [%4+%8], %1;\n\t"
+      "@pa st.shared.u32 [%4+%9], %2;\n\t"
+      "@pa st.shared.u32 [%4+%10], %3;\n\t"
+      "@pa add.u32 %4, %4, %7;\n\t"
+      "sub.u32 %0, %0, p;\n\t"
+      "add.u32 %1, %1, p;\n\t"
+      "add.u32 %1, %1, %1;\n\t"
+      "add.u32 %2, %2, p;\n\t"
+      "shr.u32 %2, %2, 1;\n\t"
+      "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"
+      "shr.u32 na, na, 31;\n\t"
+      "add.u32 %6, %6, na;\n\t"
+      "setp.eq.and.u32 ps, %0, 0, pk;\n\t"
+      "@ps add.u32 %5, %5, 1;\n\t"
+      "setp.eq.and.u32 po, %3, 0, pk;\n\t"
+      "@po sub.u32 %4, %4, %7;\n\t"
+      "@po ld.shared.u32 %0, [%4];\n\t"
+      "@po ld.shared.u32 %1, [%4+%8];\n\t"
+      "@po ld.shared.u32 %2, [%4+%9];\n\t"
+      "@po ld.shared.u32 %3, [%4+%10];\n\t"
+      "}"
+      : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+      : "n"(STRIDE), "n"(P), "n"(2 * P), "n"(3 * P)
+      : "memory");
+}
+
 struct LabParams {
   DfsParams P;
   uint32_t one, two;
@@ -171,10 +216,16 @@ __global__ void __launch_bounds__(BLOCK) lab_kernel(LabParams LP) {
   extern __shared__ uint4 stk[];
   constexpr uint32_t STRIDE = BLOCK * 16u;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t base0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) + threadIdx.x * 16u;
+  const uint32_t base0 = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) +
+                        threadIdx.x * (MODE == 5 ? 4u : 16u);
   const uint32_t base1 = base0 + STRIDE;
   constexpr uint32_t IDLE_C = MODE >= 4 ? 0u : kIdleC;  // AD: no free column when idle
-  sts128(base0, IDLE_C, kIdleL, 0u, 0u);
+  if constexpr (MODE == 5) {
+    for (int w = 0; w < 4; ++w)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(base0 + w * (STRIDE / 4)), "r"(w == 1 ? kIdleL : (w == 0 ? IDLE_C : 0u)) : "memory");
+  } else {
+    sts128(base0, IDLE_C, kIdleL, 0u, 0u);
+  }
   uint32_t C = IDLE_C, l = kIdleL, r = 0u, a = 0u, sp = base1, sol = 0u, its = 0u, weight = 0u;
   const uint32_t one = LP.one, two = LP.two;
   bool busy = false, exhausted = false;
@@ -229,7 +280,8 @@ __global__ void __launch_bounds__(BLOCK) lab_kernel(LabParams LP) {
     }
 #pragma unroll
     for (int k = 0; k < KSTEP; ++k) {
-      if constexpr (MODE >= 4) ad_step<STRIDE>(C, l, r, a, sp, sol, its);
+      if constexpr (MODE == 5) ad32_step<STRIDE>(C, l, r, a, sp, sol, its);
+      else if constexpr (MODE >= 4) ad_step<STRIDE>(C, l, r, a, sp, sol, its);
       else lab_step<STRIDE, MODE>(C, l, r, a, sp, sol, its, one, two);
     }
     steps += KSTEP;
@@ -338,10 +390,13 @@ int main(int argc, char** argv) {
   const int only = argc > 4 ? std::atoi(argv[4]) : -1;
   int idx = 0;
   auto pick = [&](auto&&... xs) { if (only < 0 || only == idx) run(b, xs...); ++idx; };
-  pick("P prod k8", nq_dfs_kernel<128, 8, false>, 128, reps);
+  pick("P prod v4", nq_dfs_kernel<128, 32, false, kLayoutV4>, 128, reps);
+  pick("P prod planes", nq_dfs_kernel<128, 32, false, kLayoutPlanes>, 128, reps);
   pick("AD k8", lab_kernel<128, 8, 4>, 128, reps);
   pick("AD k32", lab_kernel<128, 32, 4>, 128, reps);
   pick("AD k32 b256", lab_kernel<256, 32, 4>, 256, reps);
   pick("AD k32 b64", lab_kernel<64, 32, 4>, 64, reps);
+  pick("AD32 k32", lab_kernel<128, 32, 5>, 128, reps);
+  pick("AD32 k16", lab_kernel<128, 16, 5>, 128, reps);
   return 0;
 }
