@@ -59,6 +59,25 @@ def load_samples():
 
 
 # ---------------------------------------------------------------------------------------
+def shard(records, rank, world):
+    """This rank's stratified shard of the frontier: records i ≡ rank (mod world). The
+    DFS order's cost rises with index, so striding balances ranks."""
+    import numpy as np
+    return np.ascontiguousarray(records[rank::world])
+
+
+def reduce_over_ranks(pg, counts, times, device):
+    """Σ of the integer counts and max of the times over ranks (pg = torch.distributed
+    or None). The only cross-rank traffic of the bench: no data-path collective."""
+    import torch
+    cnt = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=device)
+    tmax = torch.tensor([float(t) for t in times], dtype=torch.float64, device=device)
+    if pg is not None:
+        pg.all_reduce(cnt)
+        pg.all_reduce(tmax, op=pg.ReduceOp.MAX)
+    return [int(x) for x in cnt.tolist()], [float(x) for x in tmax.tolist()]
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -209,8 +228,8 @@ def main():
 
     # ---- inputs: this rank's stratified shard of the folded frontier, resident in HBM
     full = nq.generate_packed(args.n, args.pre_rows)
-    shard = np.ascontiguousarray(full[rank::world])
-    host = torch.from_numpy(shard.view(np.int32).reshape(-1, 4)).pin_memory()
+    mine = shard(full, rank, world)
+    host = torch.from_numpy(mine.view(np.int32).reshape(-1, 4)).pin_memory()
     dev = host.cuda()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -221,14 +240,14 @@ def main():
     def step_device():
         r = _lib.NqResult()
         _lib.check(_lib.lib.nq_count_device(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
-                                            ctypes.c_void_p(dev.data_ptr()), len(shard),
+                                            ctypes.c_void_p(dev.data_ptr()), len(mine),
                                             ctypes.byref(r)))
         return r
 
     def step_e2e():
         r = _lib.NqResult()
         _lib.check(_lib.lib.nq_count(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
-                                     ctypes.c_void_p(host.data_ptr()), len(shard), ctypes.byref(r)))
+                                     ctypes.c_void_p(host.data_ptr()), len(mine), ctypes.byref(r)))
         return r
 
     def barrier():
@@ -268,14 +287,8 @@ def main():
         e2e_ms = (time.perf_counter() - t0) * 1e3
 
     # ---- cross-rank reduction: Σ counts, max time (host-side; 5 numbers per rank)
-    vec = torch.tensor([nodes, sols, 0, 0], dtype=torch.float64, device="cuda")
-    tmax = torch.tensor([t_dev, e2e_ms or 0.0], dtype=torch.float64, device="cuda")
-    cnt = torch.tensor([nodes, sols], dtype=torch.int64, device="cuda")
-    if pg:
-        pg.all_reduce(cnt)
-        pg.all_reduce(tmax, op=pg.ReduceOp.MAX)
-    nodes_all, sols_all = int(cnt[0]), int(cnt[1])
-    t_dev_max, e2e_max = float(tmax[0]), float(tmax[1])
+    (nodes_all, sols_all), (t_dev_max, e2e_max) = reduce_over_ranks(
+        pg, [nodes, sols], [t_dev, e2e_ms or 0.0], "cuda")
     per_step_sols = sols_all // args.steps
     if args.n in OEIS and per_step_sols != OEIS[args.n]:
         raise SystemExit(f"count mismatch: {per_step_sols} != OEIS {OEIS[args.n]}")

@@ -119,6 +119,12 @@ int nq_generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_
                       uint64_t cap, uint64_t* total);
 /* subproblems.hpp:118-145 */
 int nq_count_subproblems(int n, int pre_rows, uint64_t* total);
+/* Deepens `count` roots to target_rows placed rows (expand_rows, subproblems.hpp:41-55,
+ * applied per root, multiplier inherited; roots already that deep are copied). out may
+ * be NULL (count only); writes min(cap, total). Cuts deep frontiers into GPU-sized
+ * records, e.g. a systematic N=27/R=7 slice expanded to R=10 for the projection. */
+int nq_expand(int n, const nq_sub* roots, uint64_t count, int target_rows, nq_sub* out,
+              uint64_t cap, uint64_t* total);
 
 /* --- partitions (scheduler.hpp:61-102) ----------------------------------------------- */
 /* ranges receives worker_count (first, last) pairs. */

@@ -116,6 +116,8 @@ _sigs = {
     "nq_generate_slice": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _u64, _u64, ctypes.c_void_p,
                                          _u64, _P(_u64)]),
     "nq_count_subproblems": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(_u64)]),
+    "nq_expand": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, _u64, ctypes.c_int, ctypes.c_void_p,
+                                 _u64, _P(_u64)]),
     "nq_solve_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64,
                                       _P(NqSolveOpts), _P(NqReport)]),
     "nq_solve": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts), _P(NqReport)]),

@@ -179,6 +179,49 @@ int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub
   return NQ_OK;
 }
 
+// Deepen a list of roots to `target` placed rows: each root's descendants at depth
+// target in DFS order (lowest column first, as expand_rows, subproblems.hpp:41-55),
+// roots in input order, multiplier inherited. A root already at depth >= target is
+// copied as-is. Used to cut very deep frontiers (N=27 slices) into GPU-sized records.
+int expand(int n, const nq_sub* roots, uint64_t count, int target, nq_sub* out, uint64_t cap,
+           uint64_t* total) {
+  if (n < 1 || n > 31)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 31], got " + std::to_string(n));
+  if (target < 1 || target >= n)
+    return set_error(NQ_ECONFIG, "target rows must satisfy 1 <= T < n (n=" + std::to_string(n) +
+                                     ", T=" + std::to_string(target) + ")");
+  if (count && !roots) return set_error(NQ_ECONFIG, "null roots");
+  const Walker w{n, mask_of(n)};
+  for (uint64_t i = 0; i < count; ++i) {
+    const nq_sub& s = roots[i];
+    const int placed = static_cast<int>(s.row & 0xffu);
+    if ((s.cols & ~w.mask) != 0u || __builtin_popcount(s.cols) != placed)
+      return set_error(NQ_ECONFIG, "root " + std::to_string(i) + " is malformed");
+  }
+  std::vector<uint64_t> off(count + 1, 0);
+  parallel_for(count, [&](size_t i) {
+    const nq_sub& s = roots[i];
+    const int placed = static_cast<int>(s.row & 0xffu);
+    off[i + 1] = placed >= target ? 1 : w.count(s.cols, s.diag, s.antidiag, placed, target);
+  });
+  for (uint64_t i = 0; i < count; ++i) off[i + 1] += off[i];
+  if (total) *total = off[count];
+  if (!out || cap == 0) return NQ_OK;
+  parallel_for(count, [&](size_t i) {
+    if (off[i] >= cap) return;
+    const nq_sub& s = roots[i];
+    const int placed = static_cast<int>(s.row & 0xffu);
+    if (placed >= target) {
+      out[off[i]] = s;
+      return;
+    }
+    uint64_t index = off[i];
+    w.emit(s.cols, s.diag, s.antidiag, placed, target, static_cast<int>(s.row >> 8), index, 1, 0,
+           out, cap);
+  });
+  return NQ_OK;
+}
+
 int count_subproblems(int n, int pre_rows, uint64_t* total) {
   return generate_slice(n, pre_rows, 1, 0, nullptr, 0, total);
 }
@@ -192,6 +235,11 @@ extern "C" int nq_generate(int n, int pre_rows, nq_sub* out, uint64_t cap, uint6
 extern "C" int nq_generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset,
                                  nq_sub* out, uint64_t cap, uint64_t* total) {
   return nqb200::generate_slice(n, pre_rows, stride, offset, out, cap, total);
+}
+
+extern "C" int nq_expand(int n, const nq_sub* roots, uint64_t count, int target_rows, nq_sub* out,
+                         uint64_t cap, uint64_t* total) {
+  return nqb200::expand(n, roots, count, target_rows, out, cap, total);
 }
 
 extern "C" int nq_count_subproblems(int n, int pre_rows, uint64_t* total) {

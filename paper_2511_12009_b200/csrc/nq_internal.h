@@ -14,6 +14,8 @@ int check_plan(int n, int pre_rows);
 int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
                    uint64_t cap, uint64_t* total);
 int count_subproblems(int n, int pre_rows, uint64_t* total);
+int expand(int n, const nq_sub* roots, uint64_t count, int target, nq_sub* out, uint64_t cap,
+           uint64_t* total);
 
 // require_feasible (stack_config.hpp:59-71): the caller's stack budget must hold the
 // required depth n - R - lastrow; the message names the smallest built-in config.

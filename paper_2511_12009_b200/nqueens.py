@@ -272,6 +272,20 @@ def generate_slice(n: int, pre_rows: int, stride: int, offset: int) -> np.ndarra
     return a
 
 
+def expand(n: int, roots: np.ndarray, target_rows: int) -> np.ndarray:
+    """Deepen packed roots to target_rows placed rows (nq_expand): each root's
+    descendants in DFS order, roots in order, multiplier inherited."""
+    roots = np.ascontiguousarray(roots, dtype=SUB_DTYPE)
+    total = ctypes.c_uint64()
+    ptr = roots.ctypes.data if len(roots) else None
+    _call(lib.nq_expand(n, ptr, len(roots), target_rows, None, 0, ctypes.byref(total)))
+    a = np.zeros(total.value, dtype=SUB_DTYPE)
+    if total.value:
+        _call(lib.nq_expand(n, ptr, len(roots), target_rows, a.ctypes.data, total.value,
+                            ctypes.byref(total)))
+    return a
+
+
 def for_each_subproblem(plan: GenerationPlan, sink: Callable[[Subproblem], None]) -> None:
     for s in unpack(generate_packed(plan.n, plan.pre_rows)):
         sink(s)

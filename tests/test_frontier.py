@@ -96,3 +96,18 @@ def test_aggregate_mirror():
         nq.aggregate(list(zip(b + b[:1], counts + counts[:1])))
     with pytest.raises(OverflowError):
         nq.aggregate([(nq.Subproblem(1, 2, 0, 1, 2), 2**63)])
+
+
+def test_expand_reproduces_deeper_frontier():
+    """nq_expand of the R-frontier to depth R' is the R'-frontier, record for record
+    (the reference stream is a DFS, so deepening each root in order preserves it)."""
+    for n, r0, r1 in ((9, 2, 5), (12, 4, 7), (13, 2, 6), (15, 5, 8)):  # r0 >= 2: odd-N centre fold
+        got = nq.expand(n, nq.generate_packed(n, r0), r1)
+        assert np.array_equal(got, nq.generate_packed(n, r1)), (n, r0, r1)
+    a = nq.generate_packed(11, 6)
+    assert np.array_equal(nq.expand(11, a, 4), a)  # already deep enough: copied
+    assert len(nq.expand(11, a[:0], 8)) == 0
+    bad = a[:3].copy()
+    bad["row"][1] += 1  # popcount(cols) != placed_rows
+    with pytest.raises(nq.ConfigError):
+        nq.expand(11, bad, 8)

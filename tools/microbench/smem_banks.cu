@@ -24,12 +24,13 @@ __device__ __forceinline__ uint32_t hash(uint32_t x) {
 }
 
 // mode: bit0 = random level per lane (else level 0); bits1-2: active set
-//   0 = all lanes, 1 = ~37% random, 2 = lanes {0, 8}, 3 = lanes {0, 1}
+//   0 = all lanes, 1 = ~37% random, 2 = lanes {0, 8}, 3 = lanes {0, 1};
+//   bit3: padded rows (level stride BLOCK+1 frames: lane t's bank group rotates with L)
 template <int MODE, bool LOAD>
 __global__ void __launch_bounds__(BLOCK) pattern(uint32_t* out, uint32_t seed) {
-  __shared__ uint4 stk[LEVELS * BLOCK];
+  __shared__ uint4 stk[LEVELS * (BLOCK + 1)];
   const uint32_t t = threadIdx.x, lane = t & 31u;
-  for (int i = t; i < LEVELS * BLOCK; i += BLOCK) stk[i] = make_uint4(i, i, i, i);
+  for (int i = t; i < LEVELS * (BLOCK + 1); i += BLOCK) stk[i] = make_uint4(i, i, i, i);
   __syncthreads();
   const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(stk)) + t * 16u;
   uint32_t acc = 0;
@@ -38,13 +39,13 @@ __global__ void __launch_bounds__(BLOCK) pattern(uint32_t* out, uint32_t seed) {
     const uint32_t h = hash(seed ^ (it * 131u) ^ (t * 7919u));
     const uint32_t level = (MODE & 1) ? (h % LEVELS) : 0u;
     bool active;
-    switch (MODE >> 1) {
+    switch ((MODE >> 1) & 3) {
       case 0: active = true; break;
       case 1: active = (h >> 8) % 100u < 37u; break;
       case 2: active = lane == 0u || lane == 8u; break;
       default: active = lane == 0u || lane == 1u; break;
     }
-    const uint32_t addr = base + level * BLOCK * 16u;
+    const uint32_t addr = base + level * ((MODE & 8) ? (BLOCK + 1) : BLOCK) * 16u;
     if (LOAD) {
       uint32_t x = 0, y = 0, z = 0, w = 0;
       asm volatile(
@@ -82,6 +83,9 @@ int main() {
   run<5>(out);  // lanes {0,8}, random levels
   run<6>(out);  // lanes {0,1}, same level
   run<7>(out);  // lanes {0,1}, random levels
+  run<11>(out);  // padded: 37% lanes, random levels
+  run<13>(out);  // padded: lanes {0,8}, random levels
+  run<9>(out);   // padded: all lanes, random levels
   cudaDeviceSynchronize();
   std::printf("patterns done: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
