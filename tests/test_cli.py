@@ -1,0 +1,40 @@
+"""The reference-style CLI (paper_2511_12009_b200/cli.py): host-side subcommands and the
+exit-code mapping of tools/nqueens_cli.cpp:28-31, :391-402."""
+import re
+import subprocess
+import sys
+
+import pytest
+
+
+def run(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2511_12009_b200.cli", *args],
+                          capture_output=True, text=True, timeout=300)
+
+
+def test_subcount_27_7_log_line():
+    out = run("subcount", "--n", "27", "--pre-rows", "7")
+    assert out.returncode == 0
+    assert re.search(r"^\[\d{4}-\d\d-\d\d \d\d:\d\d:\d\d\.\d{3}\] Use [0-9.]+ms to generate 453688251 subproblems!$",
+                     out.stdout.strip())
+
+
+@pytest.mark.parametrize("args", [
+    ("solve", "--n", "8", "--pre-rows", "9"),
+    ("solve", "--n", "10", "--config", "config9"),
+    ("solve", "--n", "10", "--kernel", "fast"),
+    ("solve", "--n", "10", "--partition", "random"),
+    ("solve", "--n", "22", "--pre-rows", "2", "--config", "config5"),
+    ("solve",),
+])
+def test_config_errors_exit_2(args):
+    assert run(*args).returncode == 2
+
+
+@pytest.mark.gpu
+def test_solve_log_and_json():
+    out = run("solve", "--n", "12", "--pre-rows", "4", "--workers", "2")
+    assert out.returncode == 0
+    assert re.search(r"n 12 queens result 14200, calc time: \[[0-9.]+ ms\]", out.stdout)
+    js = run("solve", "--n", "11", "--format", "json")
+    assert js.returncode == 0 and '"total": 2680' in js.stdout
