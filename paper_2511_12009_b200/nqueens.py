@@ -466,6 +466,32 @@ class ExecuteOptions:
     devices: Optional[Sequence[int]] = None  # GPU extension: explicit device list
 
 
+class _CancelWatch:
+    """Copies a threading.Event into the int the C scheduler polls between chunks
+    (the ExecuteOptions::cancel atomic of scheduler.hpp:252), until stopped."""
+
+    def __init__(self, event: threading.Event, flag: ctypes.c_int):
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                if event.wait(0.001):
+                    flag.value = 1
+                    return
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        self._t.join()
+
+
+def _stop_watchers(keep: list) -> None:
+    for k in keep:
+        if isinstance(k, _CancelWatch):
+            k.stop()
+
+
 def _solve_opts(opts: ExecuteOptions, keep: list):
     if opts.progress is not None or opts.resume:
         raise ConfigError("checkpoint progress/resume is not supported on the GPU path yet")
@@ -494,6 +520,7 @@ def _solve_opts(opts: ExecuteOptions, keep: list):
         keep.append(flag)
         o.cancel = ctypes.pointer(flag)
         keep.append(o.cancel)
+        keep.append(_CancelWatch(opts.cancel, flag))
     if opts.log is not None:
         sink = opts.log
         cb = _lib.NQ_LOG_FN(lambda _u, line: sink(line.decode()))
@@ -529,20 +556,26 @@ def execute_batch(n: int, pre_rows: int, batch, opts: ExecuteOptions) -> SolveRe
     keep: list = []
     o = _solve_opts(opts, keep)
     rep = _lib.NqReport()
-    _call(lib.nq_solve_batch(n, pre_rows, a.ctypes.data if len(a) else None, len(a),
-                             ctypes.byref(o), ctypes.byref(rep)))
+    try:
+        _call(lib.nq_solve_batch(n, pre_rows, a.ctypes.data if len(a) else None, len(a),
+                                 ctypes.byref(o), ctypes.byref(rep)))
+    finally:
+        _stop_watchers(keep)
     return _report(n, pre_rows, opts, rep)
 
 
 def execute(n: int, pre_rows: int, opts: ExecuteOptions) -> SolveReport:
     """scheduler.hpp:393: generate + execute_batch (n == 1 short-circuits to Q(1) = 1)."""
     _check_board(n)
+    if n > 1:
+        require_feasible(opts.config, n, pre_rows, opts.kernel is KernelVariant.lastrow)
     keep: list = []
     o = _solve_opts(opts, keep)
     rep = _lib.NqReport()
-    if n > 1:
-        require_feasible(opts.config, n, pre_rows, opts.kernel is KernelVariant.lastrow)
-    _call(lib.nq_solve(n, pre_rows, ctypes.byref(o), ctypes.byref(rep)))
+    try:
+        _call(lib.nq_solve(n, pre_rows, ctypes.byref(o), ctypes.byref(rep)))
+    finally:
+        _stop_watchers(keep)
     r = _report(n, 0 if n == 1 else pre_rows, opts, rep)
     if n == 1:
         r.workers = [WorkerStats(worker=w) for w in range(opts.plan.worker_count)]

@@ -237,3 +237,20 @@ def test_device_resident_async_path(oracle):
 def test_int_peak_measurement():
     ops, mhz = nq.measure_int_peak(0)
     assert 5e12 < ops < 1e14 and 500 < mhz < 2500
+
+
+def test_cancel_mid_run_stops_between_chunks():
+    """A cancel raised while the GPUs are counting stops dispatch at the next chunk
+    boundary (scheduler.hpp:342-355); the report says completed = False."""
+    import threading
+    import time
+    ev = threading.Event()
+    opts = nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.stealing, 2, [], 2048))
+    timer = threading.Timer(0.05, ev.set)
+    timer.start()
+    t0 = time.perf_counter()
+    rep = nq.execute(19, 6, opts)
+    timer.cancel()
+    assert not rep.completed
+    assert sum(w.processed for w in rep.workers) < rep.task_count
+    assert time.perf_counter() - t0 < 30
