@@ -6,9 +6,10 @@
 // drives one device stream (worker w runs on devices[w % G]); it hands whole index
 // ranges or chunks to the persistent sm_100a DFS kernel instead of calling count_with
 // once per subproblem, and the per-worker partial sums are multiplier-weighted on the
-// device, checked-added on the host. PartitionStrategy::guided (an addition) hands out
-// shrinking chunks from the expensive end of the stream — the GPU default in
-// nq_solve_opts, opt-in here so the reference's defaults stay as they were.
+// device, checked-added on the host. Two strategies are additions: strided (record i to
+// worker i mod W, one persistent launch per worker — the default of the C ABI) and
+// guided (shrinking chunks from the expensive end of the stream); both are opt-in here
+// so the reference's defaults stay as they were.
 //
 // Checkpoint / resume (ExecuteOptions::progress / ::resume, runner.hpp) is out of
 // scope for the GPU path: a non-empty resume vector is rejected with config_error, and
@@ -38,13 +39,14 @@
 
 namespace nqueens {
 
-enum class PartitionStrategy { uniform, weighted, stealing, guided };
+enum class PartitionStrategy { uniform, weighted, stealing, guided, strided };
 
 inline const char* to_string(PartitionStrategy s) {
     switch (s) {
         case PartitionStrategy::uniform: return "uniform";
         case PartitionStrategy::weighted: return "weighted";
         case PartitionStrategy::guided: return "guided";
+        case PartitionStrategy::strided: return "strided";
         case PartitionStrategy::stealing: break;
     }
     return "stealing";
@@ -52,7 +54,8 @@ inline const char* to_string(PartitionStrategy s) {
 
 inline PartitionStrategy partition_strategy_from(const std::string& name) {
     for (PartitionStrategy s : {PartitionStrategy::uniform, PartitionStrategy::weighted,
-                                PartitionStrategy::stealing, PartitionStrategy::guided})
+                                PartitionStrategy::stealing, PartitionStrategy::guided,
+                                PartitionStrategy::strided})
         if (name == to_string(s)) return s;
     throw config_error("unknown partition strategy '" + name + "'");
 }
@@ -248,6 +251,7 @@ inline int to_c_strategy(PartitionStrategy s) {
         case PartitionStrategy::uniform: return NQ_PARTITION_UNIFORM;
         case PartitionStrategy::weighted: return NQ_PARTITION_WEIGHTED;
         case PartitionStrategy::stealing: return NQ_PARTITION_STEALING;
+        case PartitionStrategy::strided: return NQ_PARTITION_STRIDED;
         case PartitionStrategy::guided: break;
     }
     return NQ_PARTITION_GUIDED;

@@ -70,7 +70,7 @@ class NqReport(ctypes.Structure):
                 ("worker_count", ctypes.c_int), ("workers", NqWorkerStats * MAX_WORKERS)]
 
 
-PARTITION_UNIFORM, PARTITION_WEIGHTED, PARTITION_STEALING, PARTITION_GUIDED = 0, 1, 2, 3
+PARTITION_UNIFORM, PARTITION_WEIGHTED, PARTITION_STEALING, PARTITION_GUIDED, PARTITION_STRIDED = 0, 1, 2, 3, 4
 LOG_GENERATION, LOG_START, LOG_FINISH, LOG_RESULT = 0, 1, 2, 3
 
 

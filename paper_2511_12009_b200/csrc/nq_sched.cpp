@@ -6,9 +6,11 @@
 // failure rethrown after join, and a checked final sum. Here the same W workers each
 // drive one device stream (worker w -> devices[w % G], own pooled context) and hand
 // whole ranges / chunks to the persistent DFS kernel instead of one subproblem at a
-// time. The extra GUIDED strategy is the GPU default: chunks shrink as the stream
-// drains and are taken from the expensive end first, so the devices
-// finish together.
+// time. Two GPU strategies are added: STRIDED (the default) deals record i to worker
+// i mod W and runs each worker's share as ONE persistent launch — the cost of a record
+// rises with its index, so striding balances workers statistically and
+// every device pays one tail instead of one per chunk; GUIDED hands out chunks that
+// shrink as the stream drains, from the expensive end first.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -149,12 +151,12 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
   if (!out) return set_error(NQ_ECONFIG, "null report");
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
-  o.strategy = NQ_PARTITION_GUIDED;
+  o.strategy = NQ_PARTITION_STRIDED;
   if (opts) o = *opts;
   if (o.worker_count < 0) return set_error(NQ_ECONFIG, "worker_count must be >= 1");
   if (o.strategy == NQ_PARTITION_STEALING && o.chunk == 0)
     return set_error(NQ_ECONFIG, "chunk_size must be >= 1");
-  if (o.strategy < NQ_PARTITION_UNIFORM || o.strategy > NQ_PARTITION_GUIDED)
+  if (o.strategy < NQ_PARTITION_UNIFORM || o.strategy > NQ_PARTITION_STRIDED)
     return set_error(NQ_ECONFIG, "unknown partition strategy " + std::to_string(o.strategy));
   if (int rc = require_feasible(o.stack_depth, o.config_name, n, pre_rows,
                                 o.variant == NQ_VARIANT_LASTROW))
@@ -251,7 +253,28 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
         return NQ_OK;
       };
       if (rc == NQ_OK) {
-        if (!ranges.empty()) {
+        if (o.strategy == NQ_PARTITION_STRIDED) {
+          // Gather records w, w+W, w+2W, ... and count them in one launch.
+          std::vector<nq_sub> mine;
+          mine.reserve(count / W + 1);
+          for (uint64_t i = static_cast<uint64_t>(w); i < count; i += static_cast<uint64_t>(W))
+            mine.push_back(subs[i]);
+          st.assigned = mine.size();
+          emit(o, NQ_LOG_START, w, mine.size(), count ? double(mine.size()) / double(count) : 0.0);
+          if (o.cancel && *o.cancel) {
+            interrupted.store(true);
+          } else if (!mine.empty()) {
+            nq_result r{};
+            rc = nq_count(c, n, pre_rows, o.variant, mine.data(), mine.size(), &r);
+            if (rc == NQ_OK) {
+              st.partial_sum = r.solutions;
+              st.processed = mine.size();
+              st.nodes = r.nodes;
+              st.chunks = 1;
+              st.kernel_ms = r.kernel_ms;
+            }
+          }
+        } else if (!ranges.empty()) {
           first = ranges[2 * w];
           len = ranges[2 * w + 1] - first;
           st.assigned = len;
@@ -278,7 +301,10 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
         std::lock_guard<std::mutex> lk(fail_mu);
         if (failure.empty()) {
           const uint64_t bad = c ? ctx_last_bad(c) : ~0ull;
-          std::string where = bad != ~0ull ? "subproblem " + std::to_string(first + bad)
+          const uint64_t global_bad = o.strategy == NQ_PARTITION_STRIDED
+                                          ? static_cast<uint64_t>(w) + bad * static_cast<uint64_t>(W)
+                                          : first + bad;
+          std::string where = bad != ~0ull ? "subproblem " + std::to_string(global_bad)
                                            : "chunk [" + std::to_string(first) + ", " +
                                                  std::to_string(first + len) + ")";
           failure = "worker " + std::to_string(w) + " failed on " + where + ": " + nq_last_error();
@@ -309,7 +335,7 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   if (!out) return set_error(NQ_ECONFIG, "null report");
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
-  o.strategy = NQ_PARTITION_GUIDED;
+  o.strategy = NQ_PARTITION_STRIDED;
   if (opts) o = *opts;
   if (n < 1 || n > 32)
     return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));

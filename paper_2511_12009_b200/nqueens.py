@@ -333,6 +333,7 @@ class PartitionStrategy(enum.Enum):
     weighted = _lib.PARTITION_WEIGHTED
     stealing = _lib.PARTITION_STEALING
     guided = _lib.PARTITION_GUIDED  # GPU extension: shrinking chunks, expensive end first
+    strided = _lib.PARTITION_STRIDED  # GPU extension: record i -> worker i mod W, one launch each
 
 
 def partition_strategy_from(name: str) -> PartitionStrategy:

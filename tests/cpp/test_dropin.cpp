@@ -379,7 +379,8 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   }
   const auto batch = generate({11, 3});
   for (auto strat : {PartitionStrategy::uniform, PartitionStrategy::weighted,
-                     PartitionStrategy::stealing, PartitionStrategy::guided})
+                     PartitionStrategy::stealing, PartitionStrategy::guided,
+                     PartitionStrategy::strided})
     for (int w : {1, 2, 4, 8}) {
       ExecuteOptions o;
       o.plan.strategy = strat;

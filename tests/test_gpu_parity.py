@@ -212,10 +212,11 @@ def test_empty_and_rejected_batches():
     with pytest.raises(_lib.NqError):
         ctx.count(10, 3, shallow)  # placed_rows below the declared pre_rows
     ctx.close()
-    opts = nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 2))
-    with pytest.raises(RuntimeError) as e:
-        nq.execute_batch(10, 3, bad, opts)
-    assert "failed on subproblem 5" in str(e.value)
+    for strategy in (nq.PartitionStrategy.uniform, nq.PartitionStrategy.strided):
+        opts = nq.ExecuteOptions(plan=nq.PartitionPlan(strategy, 2))
+        with pytest.raises(RuntimeError) as e:
+            nq.execute_batch(10, 3, bad, opts)
+        assert "failed on subproblem 5" in str(e.value), (strategy, str(e.value))
 
 
 def test_device_resident_async_path(oracle):
