@@ -87,6 +87,12 @@ int nq_ctx_set_tuning(nq_ctx* ctx, int block, int blocks_per_sm, int reverse_ord
 #define NQ_LAYOUT_V4 0
 #define NQ_LAYOUT_PLANES 1
 int nq_ctx_set_layout(nq_ctx* ctx, int layout);
+/* Host cancel flag (may be NULL) polled while a synchronous call waits: once it reads
+ * non-zero, the running kernel stops handing out records at its next refill (lanes
+ * finish the subtree they hold), and the call returns with result.subproblems below the
+ * batch size — the per-subproblem cancel granularity of execute_batch
+ * (scheduler.hpp:342-355). */
+int nq_ctx_set_cancel(nq_ctx* ctx, const volatile int* cancel);
 
 /* Count a batch held in HOST memory (caller-owned, pageable or pinned). Synchronous.
  * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:319-326).

@@ -100,11 +100,13 @@ struct nq_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;             // carries the cancel word while a launch runs
+  const volatile int* cancel = nullptr;    // host flag polled while waiting (may be null)
   cudaEvent_t ev_h2d = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
   uint4* d_subs = nullptr;
   size_t d_cap = 0;                        // records
-  unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals
-  unsigned long long* h_ctl = nullptr;     // pinned mirror
+  unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals, [6] stop word
+  unsigned long long* h_ctl = nullptr;     // pinned: [0..7] mirror of d_ctl, [8] stop source
   int block = 128;
   int blocks_per_sm = 0;                   // 0 = occupancy limit
   int reverse = 1;
@@ -182,6 +184,7 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.subs = reinterpret_cast<const uint4*>(dev_subs);
   P.count = count;
   P.cursor = c->d_ctl;
+  P.stop = c->d_ctl + 6;
   P.totals = c->d_ctl + 1;
   P.each_count = each_count;
   P.each_high = each_high;
@@ -202,8 +205,30 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   return NQ_OK;
 }
 
+int wait_for(nq_ctx* c) {
+  if (!c->cancel) {
+    NQ_CUDA(cudaStreamSynchronize(c->stream));
+    return NQ_OK;
+  }
+  bool sent = false;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) NQ_CUDA(q);
+    if (!sent && *c->cancel) {  // raise the device stop word behind the running kernel
+      c->h_ctl[8] = 1;
+      NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 8, sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, c->side));
+      sent = true;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  if (sent) NQ_CUDA(cudaStreamSynchronize(c->side));
+  return NQ_OK;
+}
+
 int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
-  NQ_CUDA(cudaStreamSynchronize(c->stream));
+  if (int rc = wait_for(c)) return rc;
   const unsigned long long* t = c->h_ctl + 1;
   c->last_bad = t[4] ? t[4] - 1 : ~0ull;
   if (t[4] != 0)
@@ -261,11 +286,12 @@ int nq_ctx_create(int device, nq_ctx** out) {
                                    " is not sm_100-class; this build targets sm_100a only");
   c->sms = prop.multiProcessorCount;
   NQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  NQ_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   NQ_CUDA(cudaEventCreate(&c->ev_h2d));
   NQ_CUDA(cudaEventCreate(&c->ev_k0));
   NQ_CUDA(cudaEventCreate(&c->ev_k1));
   NQ_CUDA(cudaMalloc(&c->d_ctl, 8 * sizeof(unsigned long long)));
-  NQ_CUDA(cudaMallocHost(&c->h_ctl, 8 * sizeof(unsigned long long)));
+  NQ_CUDA(cudaMallocHost(&c->h_ctl, 16 * sizeof(unsigned long long)));
   *out = c.release();
   return NQ_OK;
 }
@@ -281,6 +307,7 @@ void nq_ctx_destroy(nq_ctx* c) {
   if (c->ev_k0) cudaEventDestroy(c->ev_k0);
   if (c->ev_k1) cudaEventDestroy(c->ev_k1);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c;
 }
 
@@ -294,6 +321,12 @@ int nq_ctx_set_tuning(nq_ctx* c, int block, int blocks_per_sm, int reverse_order
   }
   c->blocks_per_sm = std::max(blocks_per_sm, 0);
   c->reverse = reverse_order ? 1 : 0;
+  return NQ_OK;
+}
+
+int nq_ctx_set_cancel(nq_ctx* c, const volatile int* cancel) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  c->cancel = cancel;
   return NQ_OK;
 }
 

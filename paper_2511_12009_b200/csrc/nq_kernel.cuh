@@ -39,6 +39,7 @@ struct DfsParams {
   const uint4* subs;                 // packed records (nq_sub)
   unsigned long long count;          // records in subs
   unsigned long long* cursor;        // device dispatch counter (zeroed per launch)
+  const unsigned long long* stop;    // non-zero: hand out no more records (cancel)
   unsigned long long* totals;        // [0] weighted, [1] raw sols, [2] iterations,
                                      // [3] subproblems, [4] first bad record + 1
   unsigned long long* each_count;    // per-record outputs (PER_SUB only)
@@ -219,7 +220,13 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         const uint32_t leader = __ffs(need) - 1u;
         const uint32_t n_need = __popc(need);
         unsigned long long first = 0ull;
-        if (lane == leader) first = atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+        if (lane == leader) {
+          // A raised stop word (host cancel, copied in on a side stream) ends dispatch
+          // at this refill: lanes finish their current subtree, nothing new is taken.
+          first = *reinterpret_cast<const volatile unsigned long long*>(P.stop)
+                      ? P.count
+                      : atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+        }
         first = __shfl_sync(0xffffffffu, first, leader);
         if (first + n_need >= P.count) exhausted = true;
         if (a == 0u) {

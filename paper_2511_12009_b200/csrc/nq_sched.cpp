@@ -240,13 +240,15 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
       uint64_t first = 0, len = 0;
       nq_ctx* c = nullptr;
       int rc = pooled_ctx(st.device, w / G, &c);
+      if (rc == NQ_OK) nq_ctx_set_cancel(c, o.cancel);
       auto run = [&](uint64_t f, uint64_t l) -> int {
         nq_result r{};
         int e = nq_count(c, n, pre_rows, o.variant, subs + f, l, &r);
         if (e) return e;
+        if (r.subproblems < l) interrupted.store(true);  // cancelled inside the launch
         if (!add_ok(st.partial_sum, r.solutions, &st.partial_sum))
           return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
-        st.processed += l;
+        st.processed += r.subproblems;
         st.nodes += r.nodes;
         st.chunks += 1;
         st.kernel_ms += r.kernel_ms;
@@ -267,8 +269,9 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
             nq_result r{};
             rc = nq_count(c, n, pre_rows, o.variant, mine.data(), mine.size(), &r);
             if (rc == NQ_OK) {
+              if (r.subproblems < mine.size()) interrupted.store(true);
               st.partial_sum = r.solutions;
-              st.processed = mine.size();
+              st.processed = r.subproblems;
               st.nodes = r.nodes;
               st.chunks = 1;
               st.kernel_ms = r.kernel_ms;
@@ -297,6 +300,7 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
         }
       }
       st.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - s0).count();
+      if (c) nq_ctx_set_cancel(c, nullptr);
       if (rc) {
         std::lock_guard<std::mutex> lk(fail_mu);
         if (failure.empty()) {

@@ -255,3 +255,23 @@ def test_cancel_mid_run_stops_between_chunks():
     assert not rep.completed
     assert sum(w.processed for w in rep.workers) < rep.task_count
     assert time.perf_counter() - t0 < 30
+
+
+def test_cancel_inside_a_running_launch():
+    """With the strided strategy each worker is ONE persistent launch; a cancel raised
+    while it runs reaches the kernel through the device stop word (nq_ctx_set_cancel):
+    dispatch stops at the next refill, lanes finish the subtree they hold."""
+    import threading
+    import time
+    batch = nq.generate_packed(20, 7)                     # ~1.6 s of work on one B200
+    ev = threading.Event()
+    opts = nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.strided, 1))
+    timer = threading.Timer(0.2, ev.set)
+    timer.start()
+    t0 = time.perf_counter()
+    rep = nq.execute_batch(20, 7, batch, opts)
+    dt = time.perf_counter() - t0
+    timer.cancel()
+    assert not rep.completed
+    assert 0 < rep.workers[0].processed < len(batch)
+    assert dt < 1.2, dt
