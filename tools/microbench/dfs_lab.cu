@@ -204,6 +204,64 @@ __device__ __forceinline__ void ad32_step(uint32_t& C, uint32_t& l, uint32_t& r,
       : "memory");
 }
 
+// Variant S ("descend or stay", stays kept in registers like the first product kernel)
+// with the pop predicate folded into one compare: a2 < p <=> (a2 == 0 && p != 0), since
+// a2 only holds candidates above p. MODE 6: two commits on the FMA pipe (IMAD by a
+// runtime 1), two as SEL; MODE 7: four SELs.
+template <uint32_t STRIDE, int MODE>
+__device__ __forceinline__ void s_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
+                                       uint32_t& sp, uint32_t& sol, uint32_t& its, uint32_t one) {
+#define S_HEAD                                   \
+  "{\n\t"                                        \
+  ".reg .u32 na, p, a2, nC, t, nl, nr, nv;\n\t"  \
+  ".reg .pred pa, pk, pd, pu, po, ps;\n\t"       \
+  "neg.s32 na, %3;\n\t"                          \
+  "and.b32 p, %3, na;\n\t"                       \
+  "setp.ne.u32 pk, p, 0;\n\t"                    \
+  "xor.b32 a2, %3, p;\n\t"                       \
+  "setp.ne.u32 pa, a2, 0;\n\t"                   \
+  "sub.u32 nC, %0, p;\n\t"                       \
+  "add.u32 t, %1, p;\n\t"                        \
+  "add.u32 nl, t, t;\n\t"                        \
+  "add.u32 t, %2, p;\n\t"                        \
+  "shr.u32 nr, t, 1;\n\t"                        \
+  "lop3.b32 nv, nC, nl, nr, 0x10;\n\t"           \
+  "setp.ne.u32 pd, nv, 0;\n\t"                   \
+  "shr.u32 na, na, 31;\n\t"                      \
+  "add.u32 %6, %6, na;\n\t"                      \
+  "setp.eq.and.u32 ps, nC, 0, pk;\n\t"           \
+  "@ps add.u32 %5, %5, 1;\n\t"                   \
+  "and.pred pu, pd, pa;\n\t"                     \
+  "@pu st.shared.v4.u32 [%4], {%0, %1, %2, a2};\n\t" \
+  "@pu add.u32 %4, %4, %8;\n\t"                  \
+  "setp.lt.and.u32 po, a2, p, !pd;\n\t"
+#define S_TAIL                                   \
+  "@po sub.u32 %4, %4, %8;\n\t"                  \
+  "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t" \
+  "}"
+  if constexpr (MODE == 6) {
+    asm volatile(S_HEAD
+                 "selp.b32 %3, nv, a2, pd;\n\t"
+                 "@pd mad.lo.u32 %0, nC, %7, 0;\n\t"
+                 "@pd mad.lo.u32 %1, nl, %7, 0;\n\t"
+                 "selp.b32 %2, nr, %2, pd;\n\t" S_TAIL
+                 : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+                 : "r"(one), "n"(STRIDE)
+                 : "memory");
+  } else {
+    asm volatile(S_HEAD
+                 "selp.b32 %3, nv, a2, pd;\n\t"
+                 "selp.b32 %0, nC, %0, pd;\n\t"
+                 "selp.b32 %1, nl, %1, pd;\n\t"
+                 "selp.b32 %2, nr, %2, pd;\n\t" S_TAIL
+                 : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+                 : "r"(one), "n"(STRIDE)
+                 : "memory");
+  }
+#undef S_HEAD
+#undef S_TAIL
+}
+
 struct LabParams {
   DfsParams P;
   uint32_t one, two;
@@ -280,7 +338,8 @@ __global__ void __launch_bounds__(BLOCK) lab_kernel(LabParams LP) {
     }
 #pragma unroll
     for (int k = 0; k < KSTEP; ++k) {
-      if constexpr (MODE == 5) ad32_step<STRIDE>(C, l, r, a, sp, sol, its);
+      if constexpr (MODE >= 6) s_step<STRIDE, MODE>(C, l, r, a, sp, sol, its, one);
+      else if constexpr (MODE == 5) ad32_step<STRIDE>(C, l, r, a, sp, sol, its);
       else if constexpr (MODE >= 4) ad_step<STRIDE>(C, l, r, a, sp, sol, its);
       else lab_step<STRIDE, MODE>(C, l, r, a, sp, sol, its, one, two);
     }
@@ -398,5 +457,7 @@ int main(int argc, char** argv) {
   pick("AD k32 b64", lab_kernel<64, 32, 4>, 64, reps);
   pick("AD32 k32", lab_kernel<128, 32, 5>, 128, reps);
   pick("AD32 k16", lab_kernel<128, 16, 5>, 128, reps);
+  pick("S fma2 k32", lab_kernel<128, 32, 6>, 128, reps);
+  pick("S sel4 k32", lab_kernel<128, 32, 7>, 128, reps);
   return 0;
 }
