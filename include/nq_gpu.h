@@ -19,6 +19,7 @@
  *   NQ_ECONFIG   (-2)  bad n / R / depth / input        ~ nqueens::config_error
  *   NQ_EOVERFLOW (-3)  64-bit count overflow            ~ std::overflow_error
  *   NQ_ECANCEL   (-4)  cancelled between chunks         (SolveReport::completed=false)
+ *   NQ_ECHECKPOINT (-5) unreadable / corrupt / foreign checkpoint ~ nqueens::checkpoint_error
  *
  * There is no CPU fallback: every counting entry point runs the sm_100a kernels and
  * fails with NQ_ECUDA when no device is usable.
@@ -37,6 +38,7 @@ extern "C" {
 #define NQ_ECONFIG (-2)
 #define NQ_EOVERFLOW (-3)
 #define NQ_ECANCEL (-4)
+#define NQ_ECHECKPOINT (-5)
 
 #define NQ_ABI_VERSION 1
 
@@ -201,6 +203,26 @@ typedef struct nq_report {
 int nq_solve_batch(int n, int pre_rows, const nq_sub* host_subs, uint64_t count,
                    const nq_solve_opts* opts, nq_report* out);
 int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out);
+
+/* --- checkpoint / resume (runner.hpp:48-212, checkpoint.hpp:21-199) -- */
+typedef struct nq_ckpt_opts {
+  const char* path;          /* checkpoint file; rewritten atomically (tmp + rename)      */
+  uint64_t chunk;            /* records per chunk; 0 = ceil(tasks / 256) (or the file's)  */
+  double flush_interval_s;   /* rewrite at most this often; 0 = after every chunk         */
+  int resume;                /* 1 = continue the run recorded in path                     */
+} nq_ckpt_opts;
+
+/* execute() with chunk-granular progress: the folded frontier is cut into fixed chunks;
+ * workers (opts->worker_count, devices as in nq_solve_batch) take pending chunks from an
+ * atomic cursor, expensive end first; every finished chunk is recorded (weighted sum,
+ * nodes). A cancel discards only the chunk in flight; completed = 0 until every chunk is
+ * recorded. Resume validates the file (checksum, identity of n, R, variant, chunk, task
+ * count) before touching a device and recounts only the missing chunks. */
+int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* opts,
+                          const nq_ckpt_opts* ck, nq_report* out);
+/* Reads a checkpoint's run parameters and progress (for `resume <file>`). */
+int nq_checkpoint_read(const char* path, int* n, int* pre_rows, uint64_t* chunks,
+                       uint64_t* done_chunks);
 
 /* --- diagnostics ------------------------------------------------------------------- */
 /* Integer-pipe peak of the current device (LOP3+IMAD 1:1 stream, all SMs), thread

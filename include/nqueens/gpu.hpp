@@ -18,6 +18,7 @@ namespace nqueens::gpu {
 
 /// Turns a non-zero nq_* status into the reference's exception types:
 /// NQ_ECONFIG → config_error, NQ_EOVERFLOW → std::overflow_error,
+/// NQ_ECHECKPOINT → checkpoint_error,
 /// anything else (NQ_ECUDA, …) → std::runtime_error.
 inline void check(int status) {
     if (status == NQ_OK) return;
@@ -25,6 +26,7 @@ inline void check(int status) {
     switch (status) {
         case NQ_ECONFIG: throw config_error(msg);
         case NQ_EOVERFLOW: throw std::overflow_error(msg);
+        case NQ_ECHECKPOINT: throw checkpoint_error(msg);
         default: throw std::runtime_error(msg);
     }
 }

@@ -11,9 +11,10 @@
 // guided (shrinking chunks from the expensive end of the stream); both are opt-in here
 // so the reference's defaults stay as they were.
 //
-// Checkpoint / resume (ExecuteOptions::progress / ::resume, runner.hpp) is out of
-// scope for the GPU path: a non-empty resume vector is rejected with config_error, and
-// a progress board receives one final commit per contiguous worker.
+// Checkpoint / resume: the reference's per-worker high-water form (ExecuteOptions::
+// progress / ::resume, runner.hpp) is replaced by chunk-granular execute_checkpointed();
+// a non-empty resume vector is rejected with config_error, and a progress board receives
+// one final commit per contiguous worker.
 #pragma once
 
 #include <array>
@@ -352,6 +353,56 @@ inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subprobl
         d.kernel_ms = s.kernel_ms;
         if (opts.progress && s.assigned)
             opts.progress->commit(w, WorkerProgress{s.processed, s.partial_sum});
+    }
+    return report;
+}
+
+/// execute() with chunk-granular checkpoint / resume (nq_solve_checkpointed): the GPU
+/// counterpart of run_with_checkpoint (runner.hpp:48-212). `chunk` records per chunk
+/// (0 = automatic), the file is rewritten atomically at most every flush_interval_s.
+/// A corrupt or foreign file on resume throws checkpoint_error before any device work.
+inline SolveReport execute_checkpointed(int n, int pre_rows, const ExecuteOptions& opts,
+                                        const std::string& path, std::uint64_t chunk = 0,
+                                        double flush_interval_s = 0.0, bool resume = false) {
+    detail::check_board(n);
+    require_feasible(opts.config, n, pre_rows, opts.kernel == KernelVariant::lastrow);
+    nq_solve_opts o{};
+    o.variant = opts.kernel == KernelVariant::lastrow ? NQ_VARIANT_LASTROW : NQ_VARIANT_ITERATIVE;
+    o.worker_count = opts.plan.worker_count;
+    o.n_devices = static_cast<int>(opts.devices.size());
+    o.devices = opts.devices.empty() ? nullptr : opts.devices.data();
+    detail::CancelBridge cancel(opts.cancel);
+    o.cancel = cancel.flag();
+    o.stack_depth = opts.config.max_depth();
+    const std::string cfg_name(opts.config.name);
+    o.config_name = cfg_name.c_str();
+    nq_ckpt_opts ck{path.c_str(), chunk, flush_interval_s, resume ? 1 : 0};
+    nq_report rep{};
+    gpu::check(nq_solve_checkpointed(n, pre_rows, &o, &ck, &rep));
+    SolveReport report;
+    report.n = n;
+    report.pre_rows = pre_rows;
+    report.config_name = cfg_name;
+    report.kernel = opts.kernel;
+    report.strategy = PartitionStrategy::stealing;
+    report.worker_count = rep.worker_count;
+    report.task_count = rep.task_count;
+    report.generation_ms = rep.generation_ms;
+    report.calc_ms = rep.calc_ms;
+    report.total = rep.total;
+    report.nodes = rep.nodes;
+    report.completed = rep.completed != 0;
+    for (int w = 0; w < rep.worker_count; ++w) {
+        WorkerStats d;
+        d.worker = w;
+        d.processed = rep.workers[w].processed;
+        d.partial_sum = rep.workers[w].partial_sum;
+        d.elapsed_ms = rep.workers[w].elapsed_ms;
+        d.device = rep.workers[w].device;
+        d.nodes = rep.workers[w].nodes;
+        d.launches = rep.workers[w].chunks;
+        d.kernel_ms = rep.workers[w].kernel_ms;
+        report.workers.push_back(d);
     }
     return report;
 }

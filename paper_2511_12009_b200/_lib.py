@@ -18,6 +18,7 @@ NQ_ECUDA = -1
 NQ_ECONFIG = -2
 NQ_EOVERFLOW = -3
 NQ_ECANCEL = -4
+NQ_ECHECKPOINT = -5
 
 LAYOUT_V4, LAYOUT_PLANES = 0, 1
 
@@ -68,6 +69,11 @@ class NqReport(ctypes.Structure):
                 ("nodes", ctypes.c_uint64), ("generation_ms", ctypes.c_double),
                 ("calc_ms", ctypes.c_double), ("completed", ctypes.c_int),
                 ("worker_count", ctypes.c_int), ("workers", NqWorkerStats * MAX_WORKERS)]
+
+
+class NqCkptOpts(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_char_p), ("chunk", ctypes.c_uint64),
+                ("flush_interval_s", ctypes.c_double), ("resume", ctypes.c_int)]
 
 
 PARTITION_UNIFORM, PARTITION_WEIGHTED, PARTITION_STEALING, PARTITION_GUIDED, PARTITION_STRIDED = 0, 1, 2, 3, 4
@@ -122,6 +128,10 @@ _sigs = {
     "nq_solve_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64,
                                       _P(NqSolveOpts), _P(NqReport)]),
     "nq_solve": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts), _P(NqReport)]),
+    "nq_solve_checkpointed": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts),
+                                             _P(NqCkptOpts), _P(NqReport)]),
+    "nq_checkpoint_read": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_int), _P(ctypes.c_int),
+                                          _P(_u64), _P(_u64)]),
     "nq_partition_uniform": (ctypes.c_int, [_u64, ctypes.c_int, _P(_u64)]),
     "nq_partition_weighted": (ctypes.c_int, [_u64, _P(ctypes.c_double), ctypes.c_int, _P(_u64)]),
     "nq_format_log": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _u64, ctypes.c_double,

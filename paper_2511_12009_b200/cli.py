@@ -1,8 +1,9 @@
 """Command-line front end over the GPU path, mirroring the reference CLI
 (tools/nqueens_cli.cpp): `solve`, `subcount` and `bench` with the same option names,
 defaults, log lines and exit codes (0 ok, 2 config error, 3 overflow, 1 other), plus
-`--gpus` / `--devices`. `layout` and `resume` are out of scope (bank model and
-checkpointing are not on the counting path).
+`--gpus` / `--devices`. `solve --checkpoint FILE [--resume]` and `resume FILE` run the
+chunk-granular checkpointed count (nq_solve_checkpointed); `layout` (the analytical bank
+model) is replaced by ncu evidence and tests/test_layout_banks.py.
 
     python -m paper_2511_12009_b200.cli solve --n 20 --pre-rows 7 --workers 8 --partition guided
     python -m paper_2511_12009_b200.cli subcount --n 27 --pre-rows 7
@@ -16,7 +17,7 @@ import os
 import sys
 import time
 
-EXIT_OK, EXIT_OTHER, EXIT_CONFIG, EXIT_OVERFLOW = 0, 1, 2, 3
+EXIT_OK, EXIT_OTHER, EXIT_CONFIG, EXIT_OVERFLOW, EXIT_CHECKPOINT = 0, 1, 2, 3, 4
 
 
 def _workers(flag):
@@ -57,7 +58,17 @@ def do_solve(nq, a):
     opts = nq.ExecuteOptions(kernel=kernel, config=cfg,
                              plan=nq.PartitionPlan(strategy, workers, weights, a.chunk_size),
                              log=log, devices=devices)
-    rep = nq.execute(a.n, pre, opts)
+    if a.checkpoint:
+        cancel = _sigint_event()
+        opts.cancel = cancel
+        rep = nq.execute_checkpointed(a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
+                                      flush_interval_s=a.checkpoint_interval_s, resume=a.resume)
+        if rep.completed:
+            log(nq.log_result_line(a.n, rep.total, rep.calc_ms))
+        else:
+            log(f"interrupted: progress saved to {a.checkpoint}")
+    else:
+        rep = nq.execute(a.n, pre, opts)
     if a.format == "json":
         print(json.dumps(rep.to_json(), indent=2))
     elif a.format == "csv":
@@ -66,6 +77,23 @@ def do_solve(nq, a):
             print(f"{w.worker},{w.assigned},{w.processed},{w.partial_sum},{w.elapsed_ms}")
         print(f"total,,,{rep.total},{rep.calc_ms}")
     return EXIT_OK
+
+
+def _sigint_event():
+    """SIGINT / SIGTERM set a cancel event (nqueens_cli.cpp:24-26, :310-311)."""
+    import signal
+    import threading
+    ev = threading.Event()
+    for sig in (signal.SIGINT, signal.SIGTERM):
+        signal.signal(sig, lambda *_: ev.set())
+    return ev
+
+
+def do_resume(nq, a):
+    n, pre, chunks, done = nq.checkpoint_info(a.checkpoint)
+    print(f"resuming n={n} R={pre}: {done}/{chunks} chunks already counted", file=sys.stderr)
+    a.n, a.pre_rows, a.resume, a.checkpoint_chunk = n, pre, True, 0
+    return do_solve(nq, a)
 
 
 def do_subcount(nq, a):
@@ -126,6 +154,19 @@ def main(argv=None):
     s.add_argument("--export-subproblems", default="")
     s.add_argument("--gpus", type=int, default=0, help="use devices 0..G-1 (default: all visible)")
     s.add_argument("--devices", default="", help="explicit comma-separated device list")
+    s.add_argument("--checkpoint", default="", help="checkpoint file (chunk-granular progress)")
+    s.add_argument("--resume", action="store_true", help="continue the run in --checkpoint")
+    s.add_argument("--checkpoint-chunk", type=int, default=0, help="records per chunk (0 = auto)")
+    s.add_argument("--checkpoint-interval-s", type=float, default=30.0,
+                   help="rewrite the checkpoint at most this often")
+    rs = sub.add_parser("resume", help="continue an interrupted checkpointed run")
+    rs.add_argument("checkpoint")
+    rs.add_argument("--format", default="log", choices=["json", "csv", "log"])
+    rs.add_argument("--checkpoint-interval-s", type=float, default=30.0)
+    for k, v in (("config", "config2"), ("workers", None), ("partition", "stealing"),
+                 ("weights", ""), ("kernel", "lastrow"), ("chunk_size", 4096),
+                 ("export_subproblems", ""), ("gpus", 0), ("devices", "")):
+        rs.set_defaults(**{k: v})
     c = sub.add_parser("subcount", help="count generated subproblems")
     c.add_argument("--n", type=int, required=True)
     c.add_argument("--pre-rows", type=int, required=True)
@@ -145,13 +186,17 @@ def main(argv=None):
         return EXIT_OK if e.code == 0 else EXIT_CONFIG
     from . import nqueens as nq
     try:
-        return {"solve": do_solve, "subcount": do_subcount, "bench": do_bench}[a.cmd](nq, a)
+        return {"solve": do_solve, "subcount": do_subcount, "bench": do_bench,
+                "resume": do_resume}[a.cmd](nq, a)
     except nq.ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)
         return EXIT_CONFIG
     except OverflowError as e:
         print(f"overflow: {e}", file=sys.stderr)
         return EXIT_OVERFLOW
+    except nq.CheckpointError as e:
+        print(f"checkpoint error: {e}", file=sys.stderr)
+        return EXIT_CHECKPOINT
     except Exception as e:  # noqa: BLE001 — the reference maps everything else to 1
         print(f"error: {e}", file=sys.stderr)
         return EXIT_OTHER

@@ -35,11 +35,20 @@ class ConfigError(ValueError):
 config_error = ConfigError
 
 
+class CheckpointError(RuntimeError):
+    """nqueens::checkpoint_error (errors.hpp:16-19): unreadable, corrupt or foreign file."""
+
+
+checkpoint_error = CheckpointError
+
+
 def _raise(err: NqError):
     if err.code == _lib.NQ_ECONFIG:
         raise ConfigError(str(err)) from None
     if err.code == _lib.NQ_EOVERFLOW:
         raise OverflowError(str(err)) from None
+    if err.code == _lib.NQ_ECHECKPOINT:
+        raise CheckpointError(str(err)) from None
     raise RuntimeError(str(err)) from None
 
 
@@ -583,6 +592,39 @@ def execute(n: int, pre_rows: int, opts: ExecuteOptions) -> SolveReport:
         r.workers[0].partial_sum = 1
         r.worker_count = opts.plan.worker_count
     return r
+
+
+def execute_checkpointed(n: int, pre_rows: int, opts: ExecuteOptions, path: str, chunk: int = 0,
+                         flush_interval_s: float = 0.0, resume: bool = False) -> SolveReport:
+    """execute() with chunk-granular checkpoint/resume (nq_solve_checkpointed; the GPU
+    counterpart of run_with_checkpoint, runner.hpp:48-212). Workers take pending chunks;
+    a cancel leaves completed = False and a file a later resume=True call continues."""
+    _check_board(n)
+    require_feasible(opts.config, n, pre_rows, opts.kernel is KernelVariant.lastrow)
+    plan = opts.plan
+    o_opts = ExecuteOptions(kernel=opts.kernel, config=opts.config,
+                            plan=PartitionPlan(PartitionStrategy.stealing, plan.worker_count, [], 1),
+                            log=opts.log, cancel=opts.cancel, devices=opts.devices)
+    keep: list = []
+    o = _solve_opts(o_opts, keep)
+    ck = _lib.NqCkptOpts(str(path).encode(), chunk, flush_interval_s, 1 if resume else 0)
+    rep = _lib.NqReport()
+    try:
+        _call(lib.nq_solve_checkpointed(n, pre_rows, ctypes.byref(o), ctypes.byref(ck), ctypes.byref(rep)))
+    finally:
+        _stop_watchers(keep)
+    r = _report(n, pre_rows, o_opts, rep)
+    r.strategy = plan.strategy
+    return r
+
+
+def checkpoint_info(path: str):
+    """(n, pre_rows, chunks, done_chunks) recorded in a checkpoint file."""
+    n, r = ctypes.c_int(), ctypes.c_int()
+    chunks, done = ctypes.c_uint64(), ctypes.c_uint64()
+    _call(lib.nq_checkpoint_read(str(path).encode(), ctypes.byref(n), ctypes.byref(r),
+                                 ctypes.byref(chunks), ctypes.byref(done)))
+    return n.value, r.value, chunks.value, done.value
 
 
 def measure_int_peak(device: int = 0):

@@ -1,0 +1,102 @@
+"""Chunk-granular checkpoint / resume (nq_solve_checkpointed), after the reference's
+test_checkpoint.cpp: round trip, checksum corruption, identity mismatch, completed
+resume, and racing-cancel fault injection whose resumed total equals a clean run."""
+import os
+import random
+import threading
+
+import pytest
+
+from paper_2511_12009_b200 import nqueens as nq
+
+
+def fnv1a(data: bytes) -> str:
+    h = 0xcbf29ce484222325
+    for c in data:
+        h = ((h ^ c) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def write_ckpt(path, n, r, variant, chunk, tasks, done):
+    chunks = (tasks + chunk - 1) // chunk
+    ident = fnv1a(f"gen-v1|{n}|{r}|{variant}|{chunk}|{tasks}".encode())
+    body = f"nqb200-checkpoint 1\nidentity {ident}\nrun {n} {r} {variant} {chunk} {tasks} {chunks}\n"
+    body += "".join(f"done {i} {s} {nodes}\n" for i, (s, nodes) in sorted(done.items()))
+    with open(path, "w") as f:
+        f.write(body + f"checksum {fnv1a(body.encode())}\n")
+    return chunks
+
+
+def test_completed_checkpoint_resumes_without_a_device(tmp_path):
+    """Every chunk recorded: resume reports the recorded total and touches no GPU
+    (test_checkpoint.cpp:112-128)."""
+    n, r = 12, 4
+    tasks = nq.count_subproblems(n, r)
+    chunk = 1000
+    k = (tasks + chunk - 1) // chunk
+    # split Q(12) = 14200 over the chunks (values are opaque to the resume logic)
+    done = {i: (14200 // k + (1 if i < 14200 % k else 0), 7) for i in range(k)}
+    p = tmp_path / "c.ckpt"
+    write_ckpt(p, n, r, 1, chunk, tasks, done)
+    assert nq.checkpoint_info(p) == (n, r, k, k)
+    rep = nq.execute_checkpointed(n, r, nq.ExecuteOptions(), p, chunk=chunk, resume=True)
+    assert rep.completed and rep.total == 14200 and rep.nodes == 7 * k
+
+
+def test_corrupt_and_foreign_checkpoints_are_rejected(tmp_path):
+    n, r = 12, 4
+    tasks = nq.count_subproblems(n, r)
+    p = tmp_path / "c.ckpt"
+    write_ckpt(p, n, r, 1, 500, tasks, {0: (10, 20)})
+    text = p.read_text()
+    p.write_text(text.replace("done 0 10 20", "done 0 11 20"))   # payload edited
+    with pytest.raises(nq.CheckpointError, match="checksum"):
+        nq.execute_checkpointed(n, r, nq.ExecuteOptions(), p, resume=True)
+    p.write_text(text[: len(text) // 2])                          # truncated
+    with pytest.raises(nq.CheckpointError):
+        nq.execute_checkpointed(n, r, nq.ExecuteOptions(), p, resume=True)
+    write_ckpt(p, n, r, 1, 500, tasks, {})
+    with pytest.raises(nq.CheckpointError, match="different run"):
+        nq.execute_checkpointed(13, r, nq.ExecuteOptions(), p, resume=True)   # other n
+    with pytest.raises(nq.CheckpointError, match="different run"):
+        nq.execute_checkpointed(n, r, nq.ExecuteOptions(kernel=nq.KernelVariant.iterative), p,
+                                resume=True)
+    with pytest.raises(nq.CheckpointError):
+        nq.execute_checkpointed(n, r, nq.ExecuteOptions(), tmp_path / "missing.ckpt", resume=True)
+
+
+@pytest.mark.gpu
+def test_checkpointed_run_round_trip(tmp_path):
+    p = tmp_path / "run.ckpt"
+    rep = nq.execute_checkpointed(16, 5, nq.ExecuteOptions(plan=nq.PartitionPlan(worker_count=2)),
+                                  p, chunk=4000)
+    assert rep.completed and rep.total == 14772512
+    n, r, chunks, done = nq.checkpoint_info(p)
+    assert (n, r) == (16, 5) and chunks == done == (70906 + 3999) // 4000
+    again = nq.execute_checkpointed(16, 5, nq.ExecuteOptions(), p, resume=True)
+    assert again.completed and again.total == 14772512 and again.calc_ms < rep.calc_ms + 50
+
+
+@pytest.mark.gpu
+def test_racing_cancel_then_resume_equals_clean_run(tmp_path):
+    """acceptance.cpp:199-232 / test_checkpoint.cpp:130-169: cancel at random moments,
+    resume until complete; the total is always the clean one."""
+    rng = random.Random(1234)
+    for trial in range(6):
+        p = tmp_path / f"t{trial}.ckpt"
+        rounds = 0
+        resume = False
+        while True:
+            ev = threading.Event()
+            timer = threading.Timer(rng.uniform(0.0, 0.15), ev.set)
+            timer.start()
+            rep = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(
+                cancel=ev, plan=nq.PartitionPlan(worker_count=1 + trial % 3)), p, chunk=60000,
+                resume=resume)
+            timer.cancel()
+            rounds += 1
+            resume = True
+            if rep.completed:
+                break
+            assert rounds < 200
+        assert rep.total == 4968057848, (trial, rounds)

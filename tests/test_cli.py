@@ -38,3 +38,10 @@ def test_solve_log_and_json():
     assert re.search(r"n 12 queens result 14200, calc time: \[[0-9.]+ ms\]", out.stdout)
     js = run("solve", "--n", "11", "--format", "json")
     assert js.returncode == 0 and '"total": 2680' in js.stdout
+
+
+def test_resume_of_bad_checkpoint_exits_4(tmp_path):
+    p = tmp_path / "bad.ckpt"
+    p.write_text("nqb200-checkpoint 1\nchecksum 0\n")
+    assert run("resume", str(p)).returncode == 4
+    assert run("solve", "--n", "12", "--checkpoint", str(p), "--resume").returncode == 4

@@ -1,6 +1,6 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+
 ./tools/microbench/dfs_lab 18 6 3 > gpurun_out/lab_18_6.jsonl 2>&1
 ./tools/microbench/dfs_lab 20 7 1 > gpurun_out/lab_20_7.jsonl 2>&1
 cat gpurun_out/pytest_gpu.log gpurun_out/lab_*.jsonl

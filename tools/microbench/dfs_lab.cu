@@ -392,6 +392,7 @@ void run(const Bed& b, const char* name, void (*kern)(PT), int block, int reps) 
   LP.P.subs = b.d_subs;
   LP.P.count = b.count;
   LP.P.cursor = b.d_ctl;
+  LP.P.stop = b.d_ctl + 6;
   LP.P.totals = b.d_ctl + 1;
   LP.P.mask = (1u << b.n) - 1u;
   LP.P.n = b.n;
