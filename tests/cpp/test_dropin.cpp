@@ -422,6 +422,17 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   const auto one = execute(1, 0, ExecuteOptions{});
   CHECK(one.total == 1 && one.workers.size() == 1);
   CHECK(execute(18, 6, ExecuteOptions{}).total == 666090624ull);
+
+  // chunk-granular checkpoint round trip (nq_solve_checkpointed)
+  const std::string ck = "/tmp/nqb200_dropin_test.ckpt";
+  ExecuteOptions two;
+  two.plan.worker_count = 2;
+  const auto full = execute_checkpointed(14, 4, two, ck, 500);
+  CHECK(full.completed && full.total == 365596);
+  const auto again = execute_checkpointed(14, 4, ExecuteOptions{}, ck, 0, 0.0, true);
+  CHECK(again.completed && again.total == 365596);
+  CHECK_THROWS_AS(execute_checkpointed(15, 4, ExecuteOptions{}, ck, 0, 0.0, true), checkpoint_error);
+  std::remove(ck.c_str());
 }
 
 }  // namespace
