@@ -12,7 +12,8 @@ the stratified shard i ≡ rank (mod world) of the frontier (no data-path collec
 one all_reduce of the per-rank counts and a max of the per-rank times at the end).
 
 value  — device-resident frontier, CUDA-event time of the step on the launching stream.
-e2e    — nq_count() with the frontier in HOST memory: H2D copy + kernel + D2H, wall.
+e2e    — nq_solve_batch() (execute_batch's counterpart) with the frontier in pinned HOST
+         memory: H2D copy + kernel + result D2H inside the timed region, wall clock.
 roofline — integer-issue bound: achieved = nodes/s × 18 algorithmic int ops per node
             vs the int-op peak measured live on this GPU (LOP3+IMAD 1:1
            stream, nq_measure_int_peak).
@@ -244,11 +245,21 @@ def main():
                                             ctypes.byref(r)))
         return r
 
+    dev_list = (ctypes.c_int * 1)(local)
+    e2e_opts = _lib.NqSolveOpts()
+    e2e_opts.variant = _lib.VARIANT_LASTROW
+    e2e_opts.strategy = _lib.PARTITION_STRIDED
+    e2e_opts.worker_count = 1
+    e2e_opts.n_devices = 1
+    e2e_opts.devices = dev_list
+
     def step_e2e():
-        r = _lib.NqResult()
-        _lib.check(_lib.lib.nq_count(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
-                                     ctypes.c_void_p(host.data_ptr()), len(mine), ctypes.byref(r)))
-        return r
+        """execute_batch's GPU counterpart (nq_solve_batch) on this rank's HOST records:
+        H2D of the batch, the counting launch and the result read-back, every step."""
+        rep = _lib.NqReport()
+        _lib.check(_lib.lib.nq_solve_batch(args.n, args.pre_rows, ctypes.c_void_p(host.data_ptr()),
+                                           len(mine), ctypes.byref(e2e_opts), ctypes.byref(rep)))
+        return rep
 
     def barrier():
         torch.cuda.synchronize()
@@ -283,6 +294,8 @@ def main():
         for _ in range(args.steps):
             r = step_e2e()
             e2e_nodes += r.nodes
+            if r.total != res.solutions:  # same shard, same count, every step
+                raise SystemExit(f"e2e count mismatch: {r.total} != {res.solutions}")
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3
 

@@ -256,20 +256,27 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
       };
       if (rc == NQ_OK) {
         if (o.strategy == NQ_PARTITION_STRIDED) {
-          // Gather records w, w+W, w+2W, ... and count them in one launch.
-          std::vector<nq_sub> mine;
-          mine.reserve(count / W + 1);
-          for (uint64_t i = static_cast<uint64_t>(w); i < count; i += static_cast<uint64_t>(W))
-            mine.push_back(subs[i]);
-          st.assigned = mine.size();
-          emit(o, NQ_LOG_START, w, mine.size(), count ? double(mine.size()) / double(count) : 0.0);
+          // Gather records w, w+W, w+2W, ... and count them in one launch (a single
+          // worker counts the caller's buffer in place: no host copy).
+          std::vector<nq_sub> gathered;
+          const nq_sub* mine = subs;
+          uint64_t mine_n = count;
+          if (W > 1) {
+            gathered.reserve(count / W + 1);
+            for (uint64_t i = static_cast<uint64_t>(w); i < count; i += static_cast<uint64_t>(W))
+              gathered.push_back(subs[i]);
+            mine = gathered.data();
+            mine_n = gathered.size();
+          }
+          st.assigned = mine_n;
+          emit(o, NQ_LOG_START, w, mine_n, count ? double(mine_n) / double(count) : 0.0);
           if (o.cancel && *o.cancel) {
             interrupted.store(true);
-          } else if (!mine.empty()) {
+          } else if (mine_n) {
             nq_result r{};
-            rc = nq_count(c, n, pre_rows, o.variant, mine.data(), mine.size(), &r);
+            rc = nq_count(c, n, pre_rows, o.variant, mine, mine_n, &r);
             if (rc == NQ_OK) {
-              if (r.subproblems < mine.size()) interrupted.store(true);
+              if (r.subproblems < mine_n) interrupted.store(true);
               st.partial_sum = r.solutions;
               st.processed = r.subproblems;
               st.nodes = r.nodes;
