@@ -54,6 +54,17 @@ def ncu_traffic(n, pre_rows, world):
     return None if e is None else e["dram_bytes_per_launch"]
 
 
+def ncu_limits():
+    """The binding resource of the DFS kernel per the committed ncu capture."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_limits.json")) as f:
+            d = json.load(f)
+    except OSError:
+        return None
+    return {"resource": d["binding_resource"], "frac": d["smem_wavefronts_pct_of_peak"] / 100,
+            "alu_pipe_frac": d["alu_pipe_pct"] / 100, "source": d["capture"]}
+
+
 def load_samples():
     with open(os.path.join(REPO, "tests", "golden", "bench_samples.json")) as f:
         return json.load(f)
@@ -334,7 +345,8 @@ def main():
                                     f"all SMs, {mhz:.0f} MHz (nq_measure_int_peak)",
                      "ops_per_node": INT_OPS_PER_NODE,
                      "algorithmic": f"{INT_OPS_PER_NODE} int ops per DFS node x "
-                                    f"{nodes_all // args.steps} nodes per launch"},
+                                    f"{nodes_all // args.steps} nodes per launch",
+                     "binding_limit": ncu_limits()},
         "clocks": clk,
     }
     if e2e_ms is not None:
