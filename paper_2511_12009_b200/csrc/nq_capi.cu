@@ -363,6 +363,7 @@ int nq_collect(nq_ctx* c, nq_result* out) {
 int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
                     uint64_t count, nq_result* out) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  NvtxRange range("nq_count_device (DFS kernel + D2H)");
   if (int rc = check_args(n, pre_rows, variant)) return rc;
   NQ_CUDA(cudaSetDevice(c->device));
   if (int rc = enqueue(c, n, pre_rows, variant, dev_subs, count, false, nullptr, nullptr, nullptr))
@@ -373,6 +374,7 @@ int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* d
 int nq_count(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs, uint64_t count,
              nq_result* out) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  NvtxRange range("nq_count (H2D + DFS kernel + D2H)");
   if (int rc = check_args(n, pre_rows, variant)) return rc;
   NQ_CUDA(cudaSetDevice(c->device));
   if (int rc = ensure_capacity(c, count)) return rc;

@@ -152,6 +152,7 @@ int check_plan(int n, int pre_rows) {
 int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
                    uint64_t cap, uint64_t* total) {
   if (int rc = check_plan(n, pre_rows)) return rc;
+  NvtxRange range(out ? "nq_generate" : "nq_count_subproblems");
   if (stride == 0) return set_error(NQ_ECONFIG, "slice stride must be >= 1");
   const Walker w{n, mask_of(n)};
   std::vector<Prefix> pre;

@@ -3,9 +3,20 @@
 #include <cstdint>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "nq_gpu.h"
 
 namespace nqb200 {
+
+// NVTX range for the host phases (generation, H2D, launch + wait, worker lifetimes):
+// visible to ncu --nvtx filters and any NVTX consumer; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Records the thread-local message returned by nq_last_error(); returns code.
 int set_error(int code, const std::string& msg);

@@ -236,6 +236,8 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
       nq_worker_stats& st = out->workers[w];
       st.worker = w;
       st.device = devs[w % G];
+      const std::string range_name = "nq_solve_batch worker " + std::to_string(w);
+      NvtxRange range(range_name.c_str());
       const auto s0 = clk::now();
       uint64_t first = 0, len = 0;
       nq_ctx* c = nullptr;
