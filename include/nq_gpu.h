@@ -113,6 +113,17 @@ int nq_count_device_async(nq_ctx* ctx, int n, int pre_rows, int variant,
                           const nq_sub* dev_subs, uint64_t count);
 int nq_collect(nq_ctx* ctx, nq_result* out);
 
+/* GPU-side frontier deepening: `count` DEVICE-resident roots (on
+ * `device`) deepened to target_rows in nq_expand's order, written to dev_out (capacity
+ * cap; NULL = count only); *total = number of deepened records. Synchronous. */
+int nq_expand_device(int device, int n, const nq_sub* dev_roots, uint64_t count,
+                     int target_rows, nq_sub* dev_out, uint64_t cap, uint64_t* total);
+/* Host roots (a coarse frontier, e.g. R0 = 4) -> H2D -> deepened on the device to
+ * target_rows -> counted by the DFS kernel; only the coarse records cross PCIe.
+ * result->subproblems counts the deepened records. */
+int nq_count_expand(nq_ctx* ctx, int n, int target_rows, int variant, const nq_sub* host_roots,
+                    uint64_t count, nq_result* out);
+
 /* Per-subproblem results (unweighted counts, high-water marks as in
  * KernelResult, solver.hpp:34-41, and Alg. 3 node counts). Host buffers. This is the
  * count_with seam (solver.hpp:193) batched onto the device. */

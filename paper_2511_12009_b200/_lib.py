@@ -116,6 +116,10 @@ _sigs = {
     "nq_count_device_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_void_p, _u64]),
     "nq_collect": (ctypes.c_int, [ctypes.c_void_p, _P(NqResult)]),
+    "nq_expand_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64, ctypes.c_int,
+                                        ctypes.c_void_p, _u64, _P(_u64)]),
+    "nq_count_expand": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p, _u64, _P(NqResult)]),
     "nq_count_each": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_void_p, _u64, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p]),

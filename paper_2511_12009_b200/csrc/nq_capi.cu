@@ -388,6 +388,39 @@ int nq_count(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_sub
   return finish(c, variant, true, pre_rows, out);
 }
 
+int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub* host_roots,
+                    uint64_t count, nq_result* out) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (int rc = check_args(n, target_rows, variant)) return rc;
+  NvtxRange range("nq_count_expand (H2D roots + device deepening + DFS kernel)");
+  NQ_CUDA(cudaSetDevice(c->device));
+  NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
+  uint4* d_roots = nullptr;
+  NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), std::max<uint64_t>(count, 1) * 16,
+                          c->stream));
+  struct Free {
+    uint4* p;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } guard{d_roots, c->stream};
+  if (count)
+    NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                            c->stream));
+  NQ_CUDA(cudaStreamSynchronize(c->stream));
+  uint64_t total = 0;
+  if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
+                                target_rows, nullptr, 0, &total))
+    return rc;
+  if (int rc = ensure_capacity(c, total)) return rc;
+  if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
+                                target_rows, reinterpret_cast<nq_sub*>(c->d_subs), c->d_cap, &total))
+    return rc;
+  if (int rc = enqueue(c, n, target_rows, variant, reinterpret_cast<const nq_sub*>(c->d_subs), total,
+                       false, nullptr, nullptr, nullptr))
+    return rc;
+  return finish(c, variant, true, target_rows, out);
+}
+
 int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs,
                   uint64_t count, uint64_t* counts, int32_t* high_water, uint64_t* nodes) {
   if (!c) return set_error(NQ_ECONFIG, "null context");

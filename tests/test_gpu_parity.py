@@ -275,3 +275,37 @@ def test_cancel_inside_a_running_launch():
     assert not rep.completed
     assert 0 < rep.workers[0].processed < len(batch)
     assert dt < 1.2, dt
+
+
+def test_device_expansion_matches_host_expand():
+    """GPU-side frontier deepening (nq_expand_device) writes exactly the host nq_expand
+    stream, and nq_count_expand (coarse roots -> device deepening -> DFS) counts Q(n)."""
+    import torch
+    for n, r0, r1 in ((9, 2, 5), (13, 2, 6), (16, 4, 7), (18, 3, 7)):
+        roots = nq.generate_packed(n, r0)
+        want = nq.expand(n, roots, r1)
+        d_roots = torch.from_numpy(roots.view(np.int32).reshape(-1, 4)).cuda()
+        total = ctypes.c_uint64()
+        _lib.check(_lib.lib.nq_expand_device(0, n, ctypes.c_void_p(d_roots.data_ptr()), len(roots), r1,
+                                             None, 0, ctypes.byref(total)))
+        assert total.value == len(want)
+        d_out = torch.zeros((len(want), 4), dtype=torch.int32, device="cuda")
+        _lib.check(_lib.lib.nq_expand_device(0, n, ctypes.c_void_p(d_roots.data_ptr()), len(roots), r1,
+                                             ctypes.c_void_p(d_out.data_ptr()), len(want),
+                                             ctypes.byref(total)))
+        got = d_out.cpu().numpy().view(_lib.SUB_DTYPE).reshape(-1)
+        assert np.array_equal(got, want), (n, r0, r1)
+    c = Ctx()
+    r = _lib.NqResult()
+    roots = nq.generate_packed(18, 4)
+    _lib.check(_lib.lib.nq_count_expand(c.p, 18, 7, _lib.VARIANT_LASTROW, roots.ctypes.data, len(roots),
+                                        ctypes.byref(r)))
+    assert r.solutions == 666090624 and r.subproblems == nq.count_subproblems(18, 7)
+    assert r.nodes == 29341087800  # Appendix B, R=7
+    bad = roots.copy()
+    bad["row"][3] += 1
+    with pytest.raises(_lib.NqError) as e:
+        _lib.check(_lib.lib.nq_count_expand(c.p, 18, 7, _lib.VARIANT_LASTROW, bad.ctypes.data, len(bad),
+                                            ctypes.byref(r)))
+    assert "root 3" in str(e.value)
+    c.close()
