@@ -231,11 +231,21 @@ def main():
     from paper_2511_12009_b200 import _lib
     from paper_2511_12009_b200 import nqueens as nq
 
+    # NQB_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with gloo, so the
+    # multi-rank flow (shards, barrier, reductions, rank-0 line) runs on a one-GPU box.
+    share = os.environ.get("NQB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     pg = None
+    red_device = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+            red_device = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
 
     # ---- inputs: this rank's stratified shard of the folded frontier, resident in HBM
@@ -312,7 +322,7 @@ def main():
 
     # ---- cross-rank reduction: Σ counts, max time (host-side; 5 numbers per rank)
     (nodes_all, sols_all), (t_dev_max, e2e_max) = reduce_over_ranks(
-        pg, [nodes, sols], [t_dev, e2e_ms or 0.0], "cuda")
+        pg, [nodes, sols], [t_dev, e2e_ms or 0.0], red_device)
     per_step_sols = sols_all // args.steps
     if args.n in OEIS and per_step_sols != OEIS[args.n]:
         raise SystemExit(f"count mismatch: {per_step_sols} != OEIS {OEIS[args.n]}")
