@@ -249,8 +249,11 @@ def main():
         pg = dist
 
     # ---- inputs: this rank's stratified shard of the folded frontier, resident in HBM
-    full = nq.generate_packed(args.n, args.pre_rows)
-    mine = shard(full, rank, world)
+    n_records = nq.count_subproblems(args.n, args.pre_rows)
+    if world == 1:
+        mine = nq.generate_packed(args.n, args.pre_rows)
+    else:  # generate only this rank's stride (= shard(full, rank, world)), not the whole stream
+        mine = nq.generate_slice(args.n, args.pre_rows, world, rank)
     host = torch.from_numpy(mine.view(np.int32).reshape(-1, 4)).pin_memory()
     dev = host.cuda()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -341,7 +344,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (deterministic folded frontier; no dataset)",
         "config": {"workload": f"N={args.n} R={args.pre_rows} full-frontier count",
-                   "n": args.n, "pre_rows": args.pre_rows, "records": len(full),
+                   "n": args.n, "pre_rows": args.pre_rows, "records": n_records,
                    "solutions": per_step_sols, "nodes_per_step": nodes_all // args.steps,
                    "parallelism": f"stratified shard x{world}" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MiB write, untimed)",
@@ -361,7 +364,7 @@ def main():
     }
     if e2e_ms is not None:
         line["e2e"] = {"value": nodes_all / (e2e_max / 1e3), "unit": "nodes/s",
-                       "h2d_bytes_per_step": len(full) * 16, "d2h_bytes_per_step": 64,
+                       "h2d_bytes_per_step": n_records * 16, "d2h_bytes_per_step": 64 * world,
                        "ms_per_step": e2e_max / args.steps}
     if world == 1 and not args.no_cpu_baseline:
         samples = load_samples()

@@ -52,3 +52,16 @@ def test_two_rank_shard_and_reduce(tmp_path, world, oracle):
     for r in res:                                                # every rank sees the same sums
         assert r["total_all"] == want_total and r["nodes_all"] == want_nodes
         assert r["tmax"] == float(world)                         # max over ranks
+
+
+def test_rank_slice_equals_shard(oracle):
+    """bench.py generates a rank's records with nq_generate_slice(stride=world,
+    offset=rank); that must be exactly shard(full, rank, world)."""
+    import numpy as np
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_2511_12009_b200 import nqueens as nq
+    full = nq.generate_packed(14, 5)
+    for world in (2, 3, 8):
+        for rank in range(world):
+            assert np.array_equal(nq.generate_slice(14, 5, world, rank), bench.shard(full, rank, world))
