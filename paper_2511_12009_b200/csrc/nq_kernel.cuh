@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
             if ((s.x & ~P.mask) != 0u || __popc(s.x) != placed || placed < P.min_placed) {
               atomicCAS(P.totals + 4, 0ull, idx + 1ull);
               weight = 0u;
-            } else if ((s.x | 0u) == P.mask) {
+            } else if (s.x == P.mask) {
               sol = 1u;  // fully placed record: cur == last (solver.hpp:89, :148)
             } else {
               C = P.mask & ~s.x;

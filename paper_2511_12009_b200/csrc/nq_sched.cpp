@@ -148,6 +148,11 @@ extern "C" int nq_partition_weighted(uint64_t task_count, const double* weights,
 extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t count,
                               const nq_solve_opts* opts, nq_report* out) {
   using clk = std::chrono::steady_clock;
+  // The pooled per-device contexts are shared by every call: concurrent calls from
+  // different host threads run one after the other (the reference's execute_batch is
+  // likewise driven from one control thread).
+  static std::mutex solve_mu;
+  std::lock_guard<std::mutex> solve_lock(solve_mu);
   if (!out) return set_error(NQ_ECONFIG, "null report");
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
