@@ -309,3 +309,37 @@ def test_device_expansion_matches_host_expand():
                                             ctypes.byref(r)))
     assert "root 3" in str(e.value)
     c.close()
+
+
+def _random_deep_records(n, depth, k, rng):
+    """k random valid partial placements with `depth` queens (random descent, restarts
+    on dead ends), packed like the generator's records (multiplier 2)."""
+    mask = (1 << n) - 1
+    out = []
+    while len(out) < k:
+        cur = left = right = 0
+        for _ in range(depth):
+            v = mask & ~(cur | left | right)
+            if not v:
+                break
+            bits = [b for b in range(n) if v >> b & 1]
+            p = 1 << int(rng.choice(bits))
+            cur, left, right = cur | p, ((left | p) << 1) & 0xFFFFFFFF, (right | p) >> 1
+        else:
+            out.append((cur, left, right, depth | 2 << 8))
+    return np.array(out, dtype=np.uint32).view(_lib.SUB_DTYPE).reshape(-1)
+
+
+def test_wide_boards_n29_to_31_deep_records(oracle):
+    """Bit-31 handling (bitboard.hpp:36-44): random deep records of 29..31-column
+    boards (8 rows left to search), counted per record on the GPU vs the C oracle."""
+    rng = np.random.default_rng(31)
+    for n in (29, 30, 31):
+        pick = _random_deep_records(n, n - 8, 400, rng)
+        counts, _, nodes = nq.count_each(n, pick, nq.KernelVariant.lastrow, pre_rows=n - 8)
+        total, want_nodes, want_counts = oracle.solve_batch(n, pick, per_sub=True)
+        assert np.array_equal(counts, want_counts), n
+        assert int(nodes.sum()) == want_nodes, n
+        assert counts.sum() > 0, n
+    with pytest.raises(nq.ConfigError):
+        nq.count_each(32, _random_deep_records(32, 24, 1, rng), pre_rows=24)
