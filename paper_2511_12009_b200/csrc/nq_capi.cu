@@ -117,10 +117,12 @@ struct nq_ctx {
   bool p_h2d = false;
   uint64_t p_count = 0;
   uint64_t last_bad = ~0ull;               // index (within the batch) of a rejected record
+  uint64_t last_expanded = 0;              // records produced by the last nq_count_expand
 };
 
 namespace nqb200 {
 uint64_t ctx_last_bad(const nq_ctx* c) { return c->last_bad; }
+uint64_t ctx_last_expanded(const nq_ctx* c) { return c->last_expanded; }
 }  // namespace nqb200
 
 namespace {
@@ -411,6 +413,7 @@ int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub
   if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
                                 target_rows, nullptr, 0, &total))
     return rc;
+  c->last_expanded = total;
   if (int rc = ensure_capacity(c, total)) return rc;
   if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
                                 target_rows, reinterpret_cast<nq_sub*>(c->d_subs), c->d_cap, &total))

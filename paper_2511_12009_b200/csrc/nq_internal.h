@@ -36,4 +36,13 @@ int require_feasible(int stack_depth, const char* config_name, int n, int pre_ro
 // Index (within the last batch) of the record a counting call rejected, or ~0.
 uint64_t ctx_last_bad(const nq_ctx* c);
 
+// Records the last nq_count_expand deepened (the launch's full work, for cancel checks).
+uint64_t ctx_last_expanded(const nq_ctx* c);
+
+// execute_batch over records that are deepened to `target_rows` on the device first
+// (target_rows == 0: count the records as they are). nq_solve_batch is the
+// target_rows == 0 case; nq_solve uses the deepening form for large frontiers.
+int solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs, uint64_t count,
+                     const nq_solve_opts* opts, nq_report* out);
+
 }  // namespace nqb200

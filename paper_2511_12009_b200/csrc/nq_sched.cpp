@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <memory>
@@ -147,6 +148,11 @@ extern "C" int nq_partition_weighted(uint64_t task_count, const double* weights,
 
 extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t count,
                               const nq_solve_opts* opts, nq_report* out) {
+  return solve_batch_impl(n, pre_rows, 0, subs, count, opts, out);
+}
+
+int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs,
+                             uint64_t count, const nq_solve_opts* opts, nq_report* out) {
   using clk = std::chrono::steady_clock;
   // The pooled per-device contexts are shared by every call: concurrent calls from
   // different host threads run one after the other (the reference's execute_batch is
@@ -163,9 +169,12 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
     return set_error(NQ_ECONFIG, "chunk_size must be >= 1");
   if (o.strategy < NQ_PARTITION_UNIFORM || o.strategy > NQ_PARTITION_STRIDED)
     return set_error(NQ_ECONFIG, "unknown partition strategy " + std::to_string(o.strategy));
-  if (int rc = require_feasible(o.stack_depth, o.config_name, n, pre_rows,
+  if (int rc = require_feasible(o.stack_depth, o.config_name, n,
+                                target_rows ? target_rows : pre_rows,
                                 o.variant == NQ_VARIANT_LASTROW))
     return rc;
+  if (target_rows && o.strategy != NQ_PARTITION_STRIDED)
+    return set_error(NQ_ECONFIG, "device-side deepening needs the strided strategy");
   if (n < 1 || n > 31)
     return set_error(NQ_ECONFIG, "board size must be in [1, 31] on the GPU path, got " +
                                      std::to_string(n));
@@ -281,9 +290,15 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
             interrupted.store(true);
           } else if (mine_n) {
             nq_result r{};
-            rc = nq_count(c, n, pre_rows, o.variant, mine, mine_n, &r);
+            uint64_t work = mine_n;
+            if (target_rows) {  // coarse roots: deepened and counted on the device
+              rc = nq_count_expand(c, n, target_rows, o.variant, mine, mine_n, &r);
+              work = ctx_last_expanded(c);
+            } else {
+              rc = nq_count(c, n, pre_rows, o.variant, mine, mine_n, &r);
+            }
             if (rc == NQ_OK) {
-              if (r.subproblems < mine_n) interrupted.store(true);
+              if (r.subproblems < work) interrupted.store(true);
               st.partial_sum = r.solutions;
               st.processed = r.subproblems;
               st.nodes = r.nodes;
@@ -370,6 +385,26 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   const auto g0 = clk::now();
   uint64_t total = 0;
   if (int rc = count_subproblems(n, pre_rows, &total)) return rc;
+  // Large frontiers (N=27, R=7: 453,688,251 records, 7.26 GB) are never materialised on
+  // the host: a coarse frontier 3 rows shallower is dealt to the workers and deepened on
+  // each device (nq_count_expand). Threshold: NQB_DEVICE_EXPAND_MIN_RECORDS (default 2^26).
+  uint64_t expand_min = 1ull << 26;
+  if (const char* e = std::getenv("NQB_DEVICE_EXPAND_MIN_RECORDS")) expand_min = std::strtoull(e, nullptr, 10);
+  const int coarse = std::max(2, pre_rows - 3);
+  if (total >= expand_min && o.strategy == NQ_PARTITION_STRIDED && coarse < pre_rows) {
+    uint64_t roots_n = 0;
+    if (int rc = count_subproblems(n, coarse, &roots_n)) return rc;
+    std::vector<nq_sub> roots(roots_n);
+    if (int rc = generate_slice(n, coarse, 1, 0, roots.data(), roots_n, &roots_n)) return rc;
+    const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
+    emit(o, NQ_LOG_GENERATION, 0, total, gen_ms);
+    const int rc = solve_batch_impl(n, coarse, pre_rows, roots.data(), roots_n, &o, out);
+    if (rc) return rc;
+    out->task_count = total;
+    out->generation_ms = gen_ms;
+    if (out->completed) emit(o, NQ_LOG_RESULT, n, out->total, out->calc_ms);
+    return NQ_OK;
+  }
   std::vector<nq_sub> batch(total);
   if (int rc = generate_slice(n, pre_rows, 1, 0, batch.data(), total, &total)) return rc;
   const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();

@@ -343,3 +343,19 @@ def test_wide_boards_n29_to_31_deep_records(oracle):
         assert counts.sum() > 0, n
     with pytest.raises(nq.ConfigError):
         nq.count_each(32, _random_deep_records(32, 24, 1, rng), pre_rows=24)
+
+
+def test_execute_deepens_large_frontiers_on_the_device(monkeypatch, golden):
+    """nq_solve deals a coarse frontier (R-3) to the workers and deepens it on each
+    device once the R-frontier passes NQB_DEVICE_EXPAND_MIN_RECORDS (default 2^26, e.g.
+    N=27 R=7): same total and the same Alg. 3 node count as the host path."""
+    monkeypatch.setenv("NQB_DEVICE_EXPAND_MIN_RECORDS", "1000")
+    for workers in (1, 3):
+        opts = nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.strided, workers))
+        rep = nq.execute(16, 6, opts)
+        assert rep.completed and rep.total == 14772512
+        assert rep.nodes == golden["appendix_b_nodes"]["16"]["6"]
+        assert rep.task_count == nq.count_subproblems(16, 6)
+        assert sum(w.processed for w in rep.workers) == rep.task_count
+    monkeypatch.setenv("NQB_DEVICE_EXPAND_MIN_RECORDS", str(1 << 62))
+    assert nq.execute(16, 6, nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.strided, 1))).total == 14772512
