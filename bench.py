@@ -216,13 +216,20 @@ def main():
     ap.add_argument("--cpu-stride", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-mode", default="batch", choices=["batch", "expand"],
+                    help="batch: nq_solve_batch on the host R-frontier shard; expand: the "
+                         "coarse (R-3) frontier shard over PCIe, deepened on the device "
+                         "(nq_count_expand)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.pre_rows is None:
         # R=7: 22.8 M finer subtrees keep every lane busy to the end (lane efficiency
         # 99.7% vs 97.9% at R=6, tools/microbench/dfs_lab.cu) and the shallower stack
         # fits one more block per SM.
-        args.pre_rows = 7 if args.n >= 19 else 6
+        # With 4+ ranks each GPU holds 1/k of the frontier; R=8 keeps ~150 records per
+        # lane so the per-GPU tail stays short (tools/scaling_emulation.py: 8-way
+        # efficiency 95.1% at R=7, 99.1% at R=8; one GPU is equally fast at both).
+        args.pre_rows = (8 if world >= 4 else 7) if args.n >= 19 else 6
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -277,13 +284,28 @@ def main():
     e2e_opts.n_devices = 1
     e2e_opts.devices = dev_list
 
+    coarse = max(2, args.pre_rows - 3)
+    if args.e2e_mode == "expand":
+        roots = nq.generate_slice(args.n, coarse, world, rank)
+        host_roots = torch.from_numpy(roots.view(np.int32).reshape(-1, 4)).pin_memory()
+        e2e_h2d_bytes = nq.count_subproblems(args.n, coarse) * 16
+    else:
+        e2e_h2d_bytes = n_records * 16
+
     def step_e2e():
-        """execute_batch's GPU counterpart (nq_solve_batch) on this rank's HOST records:
-        H2D of the batch, the counting launch and the result read-back, every step."""
+        """Host inputs -> device -> count -> result read-back, every step. batch:
+        execute_batch's GPU counterpart (nq_solve_batch) on this rank's host R-records;
+        expand: this rank's coarse records, deepened and counted on the device."""
+        if args.e2e_mode == "expand":
+            r = _lib.NqResult()
+            _lib.check(_lib.lib.nq_count_expand(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
+                                                ctypes.c_void_p(host_roots.data_ptr()), len(roots),
+                                                ctypes.byref(r)))
+            return r.solutions, r.nodes
         rep = _lib.NqReport()
         _lib.check(_lib.lib.nq_solve_batch(args.n, args.pre_rows, ctypes.c_void_p(host.data_ptr()),
                                            len(mine), ctypes.byref(e2e_opts), ctypes.byref(rep)))
-        return rep
+        return rep.total, rep.nodes
 
     def barrier():
         torch.cuda.synchronize()
@@ -315,20 +337,25 @@ def main():
         barrier()
         t0 = time.perf_counter()
         e2e_nodes = 0
+        e2e_sols = set()
         for _ in range(args.steps):
-            r = step_e2e()
-            e2e_nodes += r.nodes
-            if r.total != res.solutions:  # same shard, same count, every step
-                raise SystemExit(f"e2e count mismatch: {r.total} != {res.solutions}")
+            sols_e2e, nodes_e2e = step_e2e()
+            e2e_nodes += nodes_e2e
+            e2e_sols.add(sols_e2e)
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3
+        if len(e2e_sols) != 1:
+            raise SystemExit(f"e2e counts differ between steps: {sorted(e2e_sols)}")
 
     # ---- cross-rank reduction: Σ counts, max time (host-side; 5 numbers per rank)
-    (nodes_all, sols_all), (t_dev_max, e2e_max) = reduce_over_ranks(
-        pg, [nodes, sols], [t_dev, e2e_ms or 0.0], red_device)
+    e2e_sol = next(iter(e2e_sols)) if e2e_ms is not None else 0
+    (nodes_all, sols_all, e2e_sol_all), (t_dev_max, e2e_max) = reduce_over_ranks(
+        pg, [nodes, sols, e2e_sol], [t_dev, e2e_ms or 0.0], red_device)
     per_step_sols = sols_all // args.steps
     if args.n in OEIS and per_step_sols != OEIS[args.n]:
         raise SystemExit(f"count mismatch: {per_step_sols} != OEIS {OEIS[args.n]}")
+    if e2e_ms is not None and e2e_sol_all != per_step_sols:
+        raise SystemExit(f"e2e count mismatch: {e2e_sol_all} != {per_step_sols}")
 
     if rank != 0:
         if pg:
@@ -364,7 +391,10 @@ def main():
     }
     if e2e_ms is not None:
         line["e2e"] = {"value": nodes_all / (e2e_max / 1e3), "unit": "nodes/s",
-                       "h2d_bytes_per_step": n_records * 16, "d2h_bytes_per_step": 64 * world,
+                       "h2d_bytes_per_step": e2e_h2d_bytes, "d2h_bytes_per_step": 64 * world,
+                       "mode": ("nq_count_expand: coarse R-3 frontier over PCIe, deepened on the device"
+                                if args.e2e_mode == "expand" else
+                                "nq_solve_batch (execute_batch) on the host R-frontier"),
                        "ms_per_step": e2e_max / args.steps}
     if world == 1 and not args.no_cpu_baseline:
         samples = load_samples()

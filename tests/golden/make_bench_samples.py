@@ -1,7 +1,7 @@
 """Pin the bench's CPU-baseline samples: node count and weighted total of the systematic
 slices (records i ≡ 0 mod stride) of the N=20 frontier, computed with the C oracle
 (multi-threaded) and cross-checked against the reference build's total when present.
-The GPU test tests/test_gpu_parity.py::test_bench_samples re-derives them on the device.
+The GPU test tests/test_gpu_parity.py::test_bench_samples_rederived_on_device re-derives them.
 
     python tests/golden/make_bench_samples.py
 """
@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 from oracle_ctypes import Oracle, Reference, reference_available  # noqa: E402
 from paper_2511_12009_b200 import nqueens as nq  # noqa: E402
 
-PLANS = [(20, 6, 256), (20, 6, 128), (20, 7, 256), (20, 7, 128), (18, 6, 16), (16, 5, 1)]
+PLANS = [(20, 6, 256), (20, 6, 128), (20, 7, 256), (20, 7, 128), (20, 8, 256), (20, 8, 128), (18, 6, 16), (16, 5, 1)]
 
 
 def main():

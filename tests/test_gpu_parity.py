@@ -359,3 +359,20 @@ def test_execute_deepens_large_frontiers_on_the_device(monkeypatch, golden):
         assert sum(w.processed for w in rep.workers) == rep.task_count
     monkeypatch.setenv("NQB_DEVICE_EXPAND_MIN_RECORDS", str(1 << 62))
     assert nq.execute(16, 6, nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.strided, 1))).total == 14772512
+
+
+def test_bench_samples_rederived_on_device():
+    """The CPU-baseline slices bench.py times (tests/golden/bench_samples.json, pinned
+    with the C oracle) give the same weighted total and node count on the GPU."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "bench_samples.json")) as f:
+        samples = json.load(f)
+    c = Ctx()
+    for key, want in samples.items():
+        n, r, stride = map(int, key.split(","))
+        sl = nq.generate_slice(n, r, stride, 0)
+        assert len(sl) == want["records"], key
+        res = c.count(n, r, sl)
+        assert (res.solutions, res.nodes) == (want["total"], want["nodes"]), key
+    c.close()
