@@ -182,10 +182,11 @@ namespace {
                                      __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
   } while (0)
 
-struct DevBuf {
+struct DevBuf {  // stream-ordered allocation, freed on the same stream
   void* p = nullptr;
+  cudaStream_t s = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
 };
 
@@ -204,33 +205,36 @@ extern "C" int nq_expand_device(int device, int n, const nq_sub* dev_roots, uint
   if (!dev_roots) return set_error(NQ_ECONFIG, "null roots");
   NvtxRange range("nq_expand_device");
   NQX_CUDA(cudaSetDevice(device));
+  // The calling thread's own stream: no implicit sync with other workers' streams.
+  const cudaStream_t st = cudaStreamPerThread;
   const uint32_t mask = (1u << n) - 1u;
   const uint64_t tiles = (count + kScanBlock - 1) / kScanBlock;
-  DevBuf counts, sums, ctl;
-  NQX_CUDA(cudaMalloc(&counts.p, count * sizeof(unsigned long long)));
-  NQX_CUDA(cudaMalloc(&sums.p, tiles * sizeof(unsigned long long)));
-  NQX_CUDA(cudaMalloc(&ctl.p, 2 * sizeof(unsigned long long)));
+  DevBuf counts{nullptr, st}, sums{nullptr, st}, ctl{nullptr, st};
+  NQX_CUDA(cudaMallocAsync(&counts.p, count * sizeof(unsigned long long), st));
+  NQX_CUDA(cudaMallocAsync(&sums.p, tiles * sizeof(unsigned long long), st));
+  NQX_CUDA(cudaMallocAsync(&ctl.p, 2 * sizeof(unsigned long long), st));
   auto* d_counts = static_cast<unsigned long long*>(counts.p);
   auto* d_sums = static_cast<unsigned long long*>(sums.p);
   auto* d_ctl = static_cast<unsigned long long*>(ctl.p);  // [0] total, [1] first bad root
-  const unsigned long long init[2] = {0ull, ~0ull};
-  NQX_CUDA(cudaMemcpy(d_ctl, init, sizeof init, cudaMemcpyHostToDevice));
+  NQX_CUDA(cudaMemsetAsync(d_ctl, 0x00, sizeof(unsigned long long), st));
+  NQX_CUDA(cudaMemsetAsync(d_ctl + 1, 0xff, sizeof(unsigned long long), st));
   int sms = 0;
   NQX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   const int threads = 128;
   const int grid = static_cast<int>(std::min<uint64_t>((count + threads - 1) / threads,
                                                        static_cast<uint64_t>(sms) * 16));
   const auto* roots = reinterpret_cast<const uint4*>(dev_roots);
-  expand_count_kernel<<<grid, threads>>>(roots, count, mask, target_rows, d_counts, d_ctl + 1);
+  expand_count_kernel<<<grid, threads, 0, st>>>(roots, count, mask, target_rows, d_counts, d_ctl + 1);
   NQX_CUDA(cudaGetLastError());
-  scan_tiles_kernel<<<static_cast<unsigned>(tiles), kScanBlock>>>(d_counts, count, d_sums);
+  scan_tiles_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, count, d_sums);
   NQX_CUDA(cudaGetLastError());
-  scan_sums_kernel<<<1, kScanBlock>>>(d_sums, tiles, d_ctl);
+  scan_sums_kernel<<<1, kScanBlock, 0, st>>>(d_sums, tiles, d_ctl);
   NQX_CUDA(cudaGetLastError());
-  add_tile_offsets_kernel<<<static_cast<unsigned>(tiles), kScanBlock>>>(d_counts, count, d_sums);
+  add_tile_offsets_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, count, d_sums);
   NQX_CUDA(cudaGetLastError());
   unsigned long long h[2];
-  NQX_CUDA(cudaMemcpy(h, d_ctl, sizeof h, cudaMemcpyDeviceToHost));
+  NQX_CUDA(cudaMemcpyAsync(h, d_ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+  NQX_CUDA(cudaStreamSynchronize(st));
   if (h[1] != ~0ull)
     return set_error(NQ_ECONFIG, "root " + std::to_string(h[1]) +
                                      " is malformed or more than " +
@@ -240,8 +244,8 @@ extern "C" int nq_expand_device(int device, int n, const nq_sub* dev_roots, uint
   if (h[0] > cap)
     return set_error(NQ_ECONFIG, "output capacity " + std::to_string(cap) + " below the " +
                                      std::to_string(h[0]) + " deepened records");
-  expand_emit_kernel<<<grid, threads>>>(roots, count, mask, target_rows, d_counts, dev_out, h[0]);
+  expand_emit_kernel<<<grid, threads, 0, st>>>(roots, count, mask, target_rows, d_counts, dev_out, h[0]);
   NQX_CUDA(cudaGetLastError());
-  NQX_CUDA(cudaDeviceSynchronize());
+  NQX_CUDA(cudaStreamSynchronize(st));
   return NQ_OK;
 }
