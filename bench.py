@@ -401,6 +401,16 @@ def main():
                                 if args.e2e_mode == "expand" else
                                 "nq_solve_batch (execute_batch) on the host R-frontier"),
                        "ms_per_step": e2e_max / args.steps}
+    if world == 1 and not args.no_e2e:
+        # BASELINE.md §3 wall time: one warm execute() — host generation of the frontier,
+        # dispatch, the counting launch and the reduction — through nq_solve.
+        rep = _lib.NqReport()
+        _lib.check(_lib.lib.nq_solve(args.n, args.pre_rows, ctypes.byref(e2e_opts), ctypes.byref(rep)))
+        if args.n in OEIS and rep.total != OEIS[args.n]:
+            raise SystemExit(f"execute() count mismatch: {rep.total}")
+        line["execute_wall_ms"] = {"generation_ms": rep.generation_ms, "calc_ms": rep.calc_ms,
+                                   "total_ms": rep.generation_ms + rep.calc_ms,
+                                   "call": "nq_solve (execute): generate + H2D + count + D2H"}
     if world == 1 and not args.no_cpu_baseline:
         samples = load_samples()
         key = f"{args.n},{args.pre_rows},{args.cpu_stride}"
