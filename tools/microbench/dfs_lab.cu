@@ -344,6 +344,53 @@ __device__ __forceinline__ void adp_step(uint32_t& C, uint32_t& l, uint32_t& r, 
       : "memory");
 }
 
+// Variant ADZ: always-descend plus the cheapest lookahead: entering a row whose
+// next-row mask V1 = C & ~((l<<1)|(r>>1)) is empty means every candidate of the row has
+// an empty child — count them all (popc) and pop at once instead of one step each.
+// Not applied on the last row (there the placements are solutions, counted by sol).
+template <uint32_t STRIDE>
+__device__ __forceinline__ void adz_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
+                                         uint32_t& sp, uint32_t& sol, uint32_t& its) {
+  asm volatile(
+      "{\n\t"
+      ".reg .u32 na, p, l1, r1, V1, t, pc;\n\t"
+      ".reg .pred pa, pk, po, ps, pz, pn, pp;\n\t"
+      "neg.s32 na, %3;\n\t"
+      "and.b32 p, %3, na;\n\t"
+      "setp.ne.u32 pk, p, 0;\n\t"
+      "xor.b32 %3, %3, p;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\t"
+      "@pa st.shared.v4.u32 [%4], {%0, %1, %2, %3};\n\t"
+      "@pa add.u32 %4, %4, %7;\n\t"
+      "sub.u32 %0, %0, p;\n\t"
+      "add.u32 %1, %1, p;\n\t"
+      "add.u32 %1, %1, %1;\n\t"
+      "add.u32 %2, %2, p;\n\t"
+      "shr.u32 %2, %2, 1;\n\t"
+      "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"
+      "shr.u32 na, na, 31;\n\t"
+      "add.u32 %6, %6, na;\n\t"
+      "setp.eq.and.u32 ps, %0, 0, pk;\n\t"
+      "@ps add.u32 %5, %5, 1;\n\t"
+      "add.u32 l1, %1, %1;\n\t"
+      "shr.u32 r1, %2, 1;\n\t"
+      "lop3.b32 V1, %0, l1, r1, 0x10;\n\t"
+      "setp.eq.u32 pz, V1, 0;\n\t"
+      "sub.u32 t, %0, 1;\n\t"
+      "and.b32 t, %0, t;\n\t"
+      "setp.ne.and.u32 pp, t, 0, pz;\n\t"
+      "@pp popc.b32 pc, %3;\n\t"
+      "@pp add.u32 %6, %6, pc;\n\t"
+      "@pp mov.b32 %3, 0;\n\t"
+      "setp.eq.and.u32 po, %3, 0, pk;\n\t"
+      "@po sub.u32 %4, %4, %7;\n\t"
+      "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t"
+      "}"
+      : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+      : "n"(STRIDE)
+      : "memory");
+}
+
 struct LabParams {
   DfsParams P;
   uint32_t one, two;
@@ -407,6 +454,13 @@ __global__ void __launch_bounds__(BLOCK) lab_kernel(LabParams LP) {
               r = s.z;
               a = C & ~(l | r);
               if constexpr (MODE == 8) adp_prune(C, l, r, a, sol, its);
+              if constexpr (MODE == 9) {  // the same zero-V1 rule at the root row
+                const uint32_t V1 = C & ~((l << 1) | (r >> 1));
+                if (V1 == 0u && (C & (C - 1u)) != 0u) {
+                  its += __popc(a);
+                  a = 0u;
+                }
+              }
               sp = base1;
             }
             if (a == 0u) {
@@ -421,7 +475,8 @@ __global__ void __launch_bounds__(BLOCK) lab_kernel(LabParams LP) {
     }
 #pragma unroll
     for (int k = 0; k < KSTEP; ++k) {
-      if constexpr (MODE == 8) adp_step<STRIDE>(C, l, r, a, sp, sol, its);
+      if constexpr (MODE == 9) adz_step<STRIDE>(C, l, r, a, sp, sol, its);
+      else if constexpr (MODE == 8) adp_step<STRIDE>(C, l, r, a, sp, sol, its);
       else if constexpr (MODE >= 6) s_step<STRIDE, MODE>(C, l, r, a, sp, sol, its, one);
       else if constexpr (MODE == 5) ad32_step<STRIDE>(C, l, r, a, sp, sol, its);
       else if constexpr (MODE >= 4) ad_step<STRIDE>(C, l, r, a, sp, sol, its);
@@ -540,7 +595,6 @@ int main(int argc, char** argv) {
   pick("AD k32", lab_kernel<128, 32, 4>, 128, reps);
 
   pick("ADP k32", lab_kernel<128, 32, 8>, 128, reps);
-  pick("ADP k16", lab_kernel<128, 16, 8>, 128, reps);
-  pick("ADP k32 b256", lab_kernel<256, 32, 8>, 256, reps);
+  pick("ADZ k32", lab_kernel<128, 32, 9>, 128, reps);
   return 0;
 }
