@@ -5,6 +5,7 @@
 
 #include "nqueens/bitboard.hpp"
 #include "nqueens/errors.hpp"
+#include "nqueens/runner.hpp"
 #include "nqueens/scheduler.hpp"
 #include "nqueens/solver.hpp"
 #include "nqueens/stack_config.hpp"

@@ -433,6 +433,25 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   CHECK(again.completed && again.total == 365596);
   CHECK_THROWS_AS(execute_checkpointed(15, 4, ExecuteOptions{}, ck, 0, 0.0, true), checkpoint_error);
   std::remove(ck.c_str());
+
+  // runner.hpp: RunSpec / run_with_checkpoint (test_checkpoint.cpp:40-59, :171-178)
+  RunSpec spec;
+  spec.n = 13;
+  spec.pre_rows = 4;
+  spec.plan.worker_count = 2;
+  CheckpointOptions co;
+  co.path = ck;
+  co.flush_interval = 300;
+  const auto run = run_with_checkpoint(spec, co);
+  CHECK(run.completed && run.total == 73712);
+  co.resume = true;
+  CHECK(run_with_checkpoint(spec, co).total == 73712);
+  spec.plan.strategy = PartitionStrategy::stealing;
+  CHECK_THROWS_AS(run_with_checkpoint(spec, co), config_error);
+  RunSpec one;
+  one.n = 1;
+  CHECK(run_with_checkpoint(one, co).total == 1);
+  std::remove(ck.c_str());
 }
 
 }  // namespace
