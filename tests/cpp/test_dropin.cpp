@@ -448,9 +448,9 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   CHECK(run_with_checkpoint(spec, co).total == 73712);
   spec.plan.strategy = PartitionStrategy::stealing;
   CHECK_THROWS_AS(run_with_checkpoint(spec, co), config_error);
-  RunSpec one;
-  one.n = 1;
-  CHECK(run_with_checkpoint(one, co).total == 1);
+  RunSpec single;
+  single.n = 1;
+  CHECK(run_with_checkpoint(single, co).total == 1);
   std::remove(ck.c_str());
 }
 
