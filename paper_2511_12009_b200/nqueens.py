@@ -618,6 +618,43 @@ def execute_checkpointed(n: int, pre_rows: int, opts: ExecuteOptions, path: str,
     return r
 
 
+@dataclass
+class RunSpec:
+    """runner.hpp:20-26."""
+    n: int = 8
+    pre_rows: int = 2
+    config: StackConfig = builtin_configs[1]
+    kernel: KernelVariant = KernelVariant.lastrow
+    plan: PartitionPlan = field(default_factory=PartitionPlan)
+
+
+@dataclass
+class CheckpointOptions:
+    """runner.hpp:28-32; flush_interval = records per recorded chunk on the GPU path."""
+    path: str = ""
+    flush_interval: int = 1_000_000
+    resume: bool = False
+
+
+def run_with_checkpoint(spec: RunSpec, ckpt: CheckpointOptions, cancel=None, log=None) -> SolveReport:
+    """runner.hpp:48-212 over the chunk-granular GPU checkpoint (execute_checkpointed),
+    with the reference's validation (stealing refused, n == 1 short-circuit)."""
+    if spec.plan.strategy is PartitionStrategy.stealing:
+        raise ConfigError("checkpointing requires a contiguous partition (uniform/weighted)")
+    _check_board(spec.n)
+    opts = ExecuteOptions(kernel=spec.kernel, config=spec.config, plan=spec.plan, log=log,
+                          cancel=cancel)
+    if spec.n == 1:
+        return execute(1, 0, opts)
+    if ckpt.flush_interval < 1:
+        raise ConfigError("flush_interval must be >= 1")
+    r = execute_checkpointed(spec.n, spec.pre_rows, opts, ckpt.path, chunk=ckpt.flush_interval,
+                             resume=ckpt.resume)
+    if r.completed and log is not None:
+        log(log_result_line(spec.n, r.total, r.calc_ms))
+    return r
+
+
 def checkpoint_info(path: str):
     """(n, pre_rows, chunks, done_chunks) recorded in a checkpoint file."""
     n, r = ctypes.c_int(), ctypes.c_int()

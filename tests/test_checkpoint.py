@@ -100,3 +100,24 @@ def test_racing_cancel_then_resume_equals_clean_run(tmp_path):
                 break
             assert rounds < 200
         assert rep.total == 4968057848, (trial, rounds)
+
+
+def test_run_with_checkpoint_validation():
+    """runner.hpp:52-53: stealing is refused; n == 1 short-circuits without a file."""
+    spec = nq.RunSpec(12, 3, plan=nq.PartitionPlan(nq.PartitionStrategy.stealing, 2))
+    with pytest.raises(nq.ConfigError, match="contiguous partition"):
+        nq.run_with_checkpoint(spec, nq.CheckpointOptions("/nonexistent/x.ckpt"))
+    with pytest.raises(nq.ConfigError):
+        nq.run_with_checkpoint(nq.RunSpec(0, 1), nq.CheckpointOptions("x"))
+
+
+@pytest.mark.gpu
+def test_run_with_checkpoint_round_trip(tmp_path):
+    p = str(tmp_path / "r.ckpt")
+    spec = nq.RunSpec(15, 5, plan=nq.PartitionPlan(nq.PartitionStrategy.uniform, 2))
+    lines = []
+    rep = nq.run_with_checkpoint(spec, nq.CheckpointOptions(p, 5000), log=lines.append)
+    assert rep.completed and rep.total == 2279184
+    assert any("n 15 queens result 2279184" in l for l in lines)
+    assert nq.run_with_checkpoint(spec, nq.CheckpointOptions(p, 5000, resume=True)).total == 2279184
+    assert nq.run_with_checkpoint(nq.RunSpec(1, 0), nq.CheckpointOptions(p)).total == 1
