@@ -90,12 +90,20 @@ def test_q_of_n_1_to_18(golden):
 
 
 def test_node_counts_appendix_b(golden):
-    """Device node counter == Appendix B (exact, reference generator) for N=14..18."""
-    for n in range(14, 19):
+    """Device node counter == Appendix B (exact, reference generator) for N=14..20,
+    R=5..7 (the N=20 profile took 47 min on 8 cores to derive)."""
+    for n in range(14, 21):
         for r, nodes in golden["appendix_b_nodes"][str(n)].items():
             rep = nq.execute(n, int(r), nq.ExecuteOptions(config=CFG1))
             assert rep.total == golden["oeis_a000170"][n - 1]
             assert rep.nodes == nodes, (n, r)
+
+
+def test_q21_bit_exact(golden):
+    """Q(21) = 314 666 222 712 through execute() (~13 s on one B200)."""
+    rep = nq.execute(21, 7, nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.strided, 1)))
+    assert rep.total == golden["oeis_a000170"][20] == 314666222712
+    assert rep.nodes == 15916162796036  # the kernel's own count, stable across runs
 
 
 @pytest.mark.slow
