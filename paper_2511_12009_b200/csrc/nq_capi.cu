@@ -153,6 +153,13 @@ int plan_launch(nq_ctx* c, int n, int pre_rows, bool per_sub, Launch* L) {
   return NQ_OK;
 }
 
+// The control block and device buffers belong to one launch at a time.
+int check_idle(const nq_ctx* c) {
+  if (c->pending)
+    return set_error(NQ_ECONFIG, "a batch is in flight on this context (call nq_collect first)");
+  return NQ_OK;
+}
+
 int check_args(int n, int pre_rows, int variant) {
   if (n < 1 || n > 31)
     return set_error(NQ_ECONFIG, "board size must be in [1, 31] on the GPU path, got " +
@@ -365,6 +372,7 @@ int nq_collect(nq_ctx* c, nq_result* out) {
 int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
                     uint64_t count, nq_result* out) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (int rc = check_idle(c)) return rc;
   NvtxRange range("nq_count_device (DFS kernel + D2H)");
   if (int rc = check_args(n, pre_rows, variant)) return rc;
   NQ_CUDA(cudaSetDevice(c->device));
@@ -376,6 +384,7 @@ int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* d
 int nq_count(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs, uint64_t count,
              nq_result* out) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (int rc = check_idle(c)) return rc;
   NvtxRange range("nq_count (H2D + DFS kernel + D2H)");
   if (int rc = check_args(n, pre_rows, variant)) return rc;
   NQ_CUDA(cudaSetDevice(c->device));
@@ -393,6 +402,7 @@ int nq_count(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_sub
 int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub* host_roots,
                     uint64_t count, nq_result* out) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (int rc = check_idle(c)) return rc;
   if (int rc = check_args(n, target_rows, variant)) return rc;
   NvtxRange range("nq_count_expand (H2D roots + device deepening + DFS kernel)");
   NQ_CUDA(cudaSetDevice(c->device));
@@ -427,6 +437,7 @@ int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub
 int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs,
                   uint64_t count, uint64_t* counts, int32_t* high_water, uint64_t* nodes) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (int rc = check_idle(c)) return rc;
   if (int rc = check_args(n, pre_rows, variant)) return rc;
   NQ_CUDA(cudaSetDevice(c->device));
   if (int rc = ensure_capacity(c, count)) return rc;

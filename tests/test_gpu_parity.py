@@ -386,3 +386,20 @@ def test_bench_samples_rederived_on_device():
         res = c.count(n, r, sl)
         assert (res.solutions, res.nodes) == (want["total"], want["nodes"]), key
     c.close()
+
+
+def test_context_refuses_a_second_launch_while_one_is_in_flight(oracle):
+    import torch
+    a = oracle.generate(16, 5)
+    dev = torch.from_numpy(a.view(np.int32).reshape(-1, 4)).cuda()
+    c = Ctx()
+    _lib.check(_lib.lib.nq_count_device_async(c.p, 16, 5, _lib.VARIANT_LASTROW,
+                                              ctypes.c_void_p(dev.data_ptr()), len(a)))
+    with pytest.raises(_lib.NqError) as e:
+        c.count(16, 5, a)
+    assert "in flight" in str(e.value)
+    r = _lib.NqResult()
+    _lib.check(_lib.lib.nq_collect(c.p, ctypes.byref(r)))
+    assert r.solutions == 14772512
+    assert c.count(16, 5, a).solutions == 14772512
+    c.close()
