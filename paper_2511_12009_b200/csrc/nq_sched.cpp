@@ -40,7 +40,7 @@ std::string timestamp() {
   const std::time_t t = system_clock::to_time_t(now);
   std::tm tm{};
   localtime_r(&t, &tm);
-  char buf[40];
+  char buf[96];
   std::snprintf(buf, sizeof buf, "[%04d-%02d-%02d %02d:%02d:%02d.%03d]", tm.tm_year + 1900,
                 tm.tm_mon + 1, tm.tm_mday, tm.tm_hour, tm.tm_min, tm.tm_sec,
                 static_cast<int>(ms.count()));
