@@ -262,13 +262,14 @@ inline int to_c_strategy(PartitionStrategy s) {
 class CancelBridge {
 public:
     explicit CancelBridge(const std::atomic<bool>* src) : src_(src) {
-        if (src_) poller_ = std::thread([this] {
+        if (!src_) return;
+        if (src_->load()) raise();
+        poller_ = std::thread([this] {
             while (!stop_.load()) {
-                if (src_->load(std::memory_order_relaxed)) flag_ = 1;
+                if (src_->load(std::memory_order_relaxed)) raise();
                 std::this_thread::sleep_for(std::chrono::milliseconds(1));
             }
         });
-        if (src_ && src_->load()) flag_ = 1;
     }
     ~CancelBridge() {
         stop_.store(true);
@@ -277,6 +278,9 @@ public:
     const volatile int* flag() const { return src_ ? &flag_ : nullptr; }
 
 private:
+    // The library reads the flag with an atomic load (nq_internal.h: cancel_raised).
+    void raise() { __atomic_store_n(const_cast<int*>(&flag_), 1, __ATOMIC_RELAXED); }
+
     const std::atomic<bool>* src_;
     volatile int flag_ = 0;
     std::atomic<bool> stop_{false};

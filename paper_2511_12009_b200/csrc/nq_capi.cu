@@ -224,7 +224,7 @@ int wait_for(nq_ctx* c) {
     const cudaError_t q = cudaStreamQuery(c->stream);
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) NQ_CUDA(q);
-    if (!sent && *c->cancel) {  // raise the device stop word behind the running kernel
+    if (!sent && cancel_raised(c->cancel)) {  // raise the device stop word behind the running kernel
       c->h_ctl[8] = 1;
       NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 8, sizeof(unsigned long long),
                               cudaMemcpyHostToDevice, c->side));

@@ -134,6 +134,8 @@ int parse(const std::string& path, RunKey* key, std::map<uint64_t, ChunkResult>*
     }
   }
   if (!header || !have_run) return set_error(NQ_ECHECKPOINT, "checkpoint header incomplete");
+  if (key->chunk == 0 || key->chunks != (key->tasks + key->chunk - 1) / key->chunk)
+    return set_error(NQ_ECHECKPOINT, "checkpoint run line is inconsistent (chunk / chunk count)");
   if (ident != key->identity())
     return set_error(NQ_ECHECKPOINT, "checkpoint identity does not match its run line");
   for (const auto& [idx, r] : *done)
@@ -252,7 +254,7 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
       int rc = nq_ctx_create(st.device, &c);
       if (rc == NQ_OK) rc = nq_ctx_set_cancel(c, o.cancel);
       while (rc == NQ_OK && !interrupted.load()) {
-        if (o.cancel && *o.cancel) {
+        if (cancel_raised(o.cancel)) {
           interrupted.store(true);
           break;
         }

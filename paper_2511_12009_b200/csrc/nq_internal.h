@@ -18,6 +18,12 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// A caller's cancel flag (nq_solve_opts::cancel, nq_ctx_set_cancel) is written by
+// another thread: read it with an atomic load, never a plain (racy) one.
+inline bool cancel_raised(const volatile int* flag) {
+  return flag && __atomic_load_n(const_cast<const int*>(flag), __ATOMIC_RELAXED) != 0;
+}
+
 // Records the thread-local message returned by nq_last_error(); returns code.
 int set_error(int code, const std::string& msg);
 

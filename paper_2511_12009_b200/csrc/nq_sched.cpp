@@ -286,7 +286,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           }
           st.assigned = mine_n;
           emit(o, NQ_LOG_START, w, mine_n, count ? double(mine_n) / double(count) : 0.0);
-          if (o.cancel && *o.cancel) {
+          if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (mine_n) {
             nq_result r{};
@@ -311,7 +311,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           len = ranges[2 * w + 1] - first;
           st.assigned = len;
           emit(o, NQ_LOG_START, w, len, count ? double(len) / double(count) : 0.0);
-          if (o.cancel && *o.cancel) {
+          if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (len) {
             rc = run(first, len);
@@ -319,7 +319,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         } else {
           emit(o, NQ_LOG_START, w, 0, 0.0);
           while (rc == NQ_OK && !interrupted.load()) {
-            if (o.cancel && *o.cancel) {
+            if (cancel_raised(o.cancel)) {
               interrupted.store(true);
               break;
             }
