@@ -121,6 +121,10 @@ struct nq_ctx {
 };
 
 namespace nqb200 {
+// nq_expand.cu: deepen device roots to `target` rows on stream `st` into a new buffer.
+int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, int target,
+                  cudaStream_t st, uint4** out, uint64_t* total);
+
 uint64_t ctx_last_bad(const nq_ctx* c) { return c->last_bad; }
 uint64_t ctx_last_expanded(const nq_ctx* c) { return c->last_expanded; }
 }  // namespace nqb200
@@ -413,23 +417,21 @@ int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub
   struct Free {
     uint4* p;
     cudaStream_t s;
-    ~Free() { cudaFreeAsync(p, s); }
-  } guard{d_roots, c->stream};
+    ~Free() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } roots_guard{d_roots, c->stream}, deep_guard{nullptr, c->stream};
   if (count)
     NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
                             c->stream));
-  NQ_CUDA(cudaStreamSynchronize(c->stream));
   uint64_t total = 0;
-  if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
-                                target_rows, nullptr, 0, &total))
+  // Deepen on the context's own stream (ordered after the copy), then count in place.
+  if (int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
+                             target_rows, c->stream, &deep_guard.p, &total))
     return rc;
   c->last_expanded = total;
-  if (int rc = ensure_capacity(c, total)) return rc;
-  if (int rc = nq_expand_device(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
-                                target_rows, reinterpret_cast<nq_sub*>(c->d_subs), c->d_cap, &total))
-    return rc;
-  if (int rc = enqueue(c, n, target_rows, variant, reinterpret_cast<const nq_sub*>(c->d_subs), total,
-                       false, nullptr, nullptr, nullptr))
+  if (int rc = enqueue(c, n, target_rows, variant, reinterpret_cast<const nq_sub*>(deep_guard.p),
+                       total, false, nullptr, nullptr, nullptr))
     return rc;
   return finish(c, variant, true, target_rows, out);
 }

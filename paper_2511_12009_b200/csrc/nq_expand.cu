@@ -5,10 +5,10 @@
 // 453,688,251 records, 7.26 GB). Here a small coarse frontier (depth R0, shipped from
 // the host) is deepened to depth R on the device, in the same order as the host's
 // nq_expand (each root's descendants in expand_rows' DFS order, subproblems.hpp:41-55,
-// roots in order, multiplier inherited):
-//   1. one thread per root counts its depth-R descendants (bounded DFS, local frames);
+// roots in order, multiplier inherited), one row per pass:
+//   1. one thread per record counts its children (popcount of the next row's mask);
 //   2. an exclusive scan turns counts into output offsets (block scans + a carry pass);
-//   3. one thread per root writes its descendants at its offset.
+//   3. one thread per record writes its children, lowest column first, at its offset.
 // The deepened records are then counted by nq_dfs_kernel without leaving the device.
 #include <cuda_runtime.h>
 
@@ -21,65 +21,7 @@
 
 namespace nqb200 {
 
-constexpr int kExpandMaxDepth = 16;  // rows deepened per root (target - placed)
 constexpr int kScanBlock = 1024;
-
-// Walk the depth-`target` descendants of one root in DFS order (lowest column first);
-// EMIT = false counts them, EMIT = true writes them to out[at...].
-template <bool EMIT>
-__device__ uint64_t expand_one(uint4 root, uint32_t mask, int target, nq_sub* out, uint64_t at) {
-  const int placed = static_cast<int>(root.w & 0xffu);
-  if (placed >= target) {
-    if (EMIT) out[at] = nq_sub{root.x, root.y, root.z, root.w};
-    return 1;
-  }
-  const uint32_t mult = root.w & ~0xffu;
-  const int depth = target - placed;  // rows to place, <= kExpandMaxDepth
-  uint32_t cols[kExpandMaxDepth], diag[kExpandMaxDepth], anti[kExpandMaxDepth],
-      cand[kExpandMaxDepth];
-  cols[0] = root.x;
-  diag[0] = root.y;
-  anti[0] = root.z;
-  cand[0] = mask & ~(root.x | root.y | root.z);
-  int lv = 0;
-  uint64_t k = 0;
-  while (lv >= 0) {
-    const uint32_t a = cand[lv];
-    if (a == 0u) {
-      --lv;
-      continue;
-    }
-    const uint32_t p = a & (0u - a);
-    cand[lv] = a ^ p;
-    const uint32_t c = cols[lv] | p, d = (diag[lv] | p) << 1, r = (anti[lv] | p) >> 1;
-    if (lv + 1 == depth) {
-      if (EMIT) out[at + k] = nq_sub{c, d, r, static_cast<uint32_t>(target) | mult};
-      ++k;
-    } else {
-      ++lv;
-      cols[lv] = c;
-      diag[lv] = d;
-      anti[lv] = r;
-      cand[lv] = mask & ~(c | d | r);
-    }
-  }
-  return k;
-}
-
-__global__ void expand_count_kernel(const uint4* roots, uint64_t count, uint32_t mask, int target,
-                                    unsigned long long* counts, unsigned long long* bad) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint4 s = roots[i];
-    const int placed = static_cast<int>(s.w & 0xffu);
-    if ((s.x & ~mask) != 0u || __popc(s.x) != placed || target - placed > kExpandMaxDepth) {
-      atomicMin(bad, static_cast<unsigned long long>(i));
-      counts[i] = 0;
-      continue;
-    }
-    counts[i] = expand_one<false>(s, mask, target, nullptr, 0);
-  }
-}
 
 // In-place exclusive scan of each kScanBlock-element tile; tile totals to sums[tile].
 __global__ void __launch_bounds__(kScanBlock) scan_tiles_kernel(unsigned long long* v, uint64_t count,
@@ -156,15 +98,48 @@ __global__ void add_tile_offsets_kernel(unsigned long long* v, uint64_t count,
   if (i < count) v[i] += sums[blockIdx.x];
 }
 
-__global__ void expand_emit_kernel(const uint4* roots, uint64_t count, uint32_t mask, int target,
-                                   const unsigned long long* offsets, nq_sub* out, uint64_t cap) {
+// ---- level-synchronous deepening (one row per pass) ------------------------------------
+// Pass: every record below the target places one more queen (each candidate of its next
+// row, lowest column first, multiplier kept); records at the target are copied. Counts
+// -> exclusive scan -> emit keeps the DFS order of the stream; writes from one thread are
+// contiguous, so the pass streams at close to HBM speed.
+__global__ void level_count_kernel(const uint4* in, uint64_t count, uint32_t mask, int target,
+                                   unsigned long long* counts, unsigned long long* bad,
+                                   unsigned int* min_placed) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint4 s = roots[i];
-    const uint64_t at = offsets[i];
-    const uint64_t end = (i + 1 < count) ? offsets[i + 1] : cap;  // caller checked total <= cap
-    if (at >= end) continue;
-    expand_one<true>(s, mask, target, out, at);
+    const uint4 s = in[i];
+    const int placed = static_cast<int>(s.w & 0xffu);
+    if (bad) {  // first pass: validate the roots
+      if ((s.x & ~mask) != 0u || __popc(s.x) != placed) {
+        atomicMin(bad, static_cast<unsigned long long>(i));
+        counts[i] = 0;
+        continue;
+      }
+      atomicMin(min_placed, static_cast<unsigned int>(placed));
+    }
+    counts[i] = placed >= target ? 1ull : static_cast<unsigned long long>(__popc(mask & ~(s.x | s.y | s.z)));
+  }
+}
+
+__global__ void level_emit_kernel(const uint4* in, uint64_t count, uint32_t mask, int target,
+                                  const unsigned long long* offsets, uint4* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 s = in[i];
+    uint64_t at = offsets[i];
+    const int placed = static_cast<int>(s.w & 0xffu);
+    if (placed >= target) {
+      out[at] = s;
+      continue;
+    }
+    const uint32_t w = (s.w & ~0xffu) | static_cast<uint32_t>(placed + 1);
+    uint32_t v = mask & ~(s.x | s.y | s.z);
+    while (v) {
+      const uint32_t p = v & (0u - v);
+      v ^= p;
+      out[at++] = make_uint4(s.x | p, (s.y | p) << 1, (s.z | p) >> 1, w);
+    }
   }
 }
 
@@ -192,60 +167,97 @@ struct DevBuf {  // stream-ordered allocation, freed on the same stream
 
 }  // namespace
 
-extern "C" int nq_expand_device(int device, int n, const nq_sub* dev_roots, uint64_t count,
-                                int target_rows, nq_sub* dev_out, uint64_t cap, uint64_t* total) {
+namespace nqb200 {
+
+// Deepens `count` device roots to `target` rows on `st`; returns a new device buffer of
+// *total records (caller frees with cudaFreeAsync on st).
+int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, int target,
+                  cudaStream_t st, uint4** out, uint64_t* total) {
+  *out = nullptr;
+  *total = 0;
   if (n < 1 || n > 31)
     return set_error(NQ_ECONFIG, "board size must be in [1, 31], got " + std::to_string(n));
-  if (target_rows < 1 || target_rows >= n)
+  if (target < 1 || target >= n)
     return set_error(NQ_ECONFIG, "target rows must satisfy 1 <= T < n (n=" + std::to_string(n) +
-                                     ", T=" + std::to_string(target_rows) + ")");
-  if (!total) return set_error(NQ_ECONFIG, "null total");
-  *total = 0;
+                                     ", T=" + std::to_string(target) + ")");
   if (count == 0) return NQ_OK;
   if (!dev_roots) return set_error(NQ_ECONFIG, "null roots");
-  NvtxRange range("nq_expand_device");
+  NvtxRange range("nq_expand_device (level passes)");
   NQX_CUDA(cudaSetDevice(device));
-  // The calling thread's own stream: no implicit sync with other workers' streams.
-  const cudaStream_t st = cudaStreamPerThread;
   const uint32_t mask = (1u << n) - 1u;
-  const uint64_t tiles = (count + kScanBlock - 1) / kScanBlock;
-  DevBuf counts{nullptr, st}, sums{nullptr, st}, ctl{nullptr, st};
-  NQX_CUDA(cudaMallocAsync(&counts.p, count * sizeof(unsigned long long), st));
-  NQX_CUDA(cudaMallocAsync(&sums.p, tiles * sizeof(unsigned long long), st));
-  NQX_CUDA(cudaMallocAsync(&ctl.p, 2 * sizeof(unsigned long long), st));
-  auto* d_counts = static_cast<unsigned long long*>(counts.p);
-  auto* d_sums = static_cast<unsigned long long*>(sums.p);
-  auto* d_ctl = static_cast<unsigned long long*>(ctl.p);  // [0] total, [1] first bad root
-  NQX_CUDA(cudaMemsetAsync(d_ctl, 0x00, sizeof(unsigned long long), st));
-  NQX_CUDA(cudaMemsetAsync(d_ctl + 1, 0xff, sizeof(unsigned long long), st));
   int sms = 0;
   NQX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const int threads = 128;
-  const int grid = static_cast<int>(std::min<uint64_t>((count + threads - 1) / threads,
-                                                       static_cast<uint64_t>(sms) * 16));
-  const auto* roots = reinterpret_cast<const uint4*>(dev_roots);
-  expand_count_kernel<<<grid, threads, 0, st>>>(roots, count, mask, target_rows, d_counts, d_ctl + 1);
-  NQX_CUDA(cudaGetLastError());
-  scan_tiles_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, count, d_sums);
-  NQX_CUDA(cudaGetLastError());
-  scan_sums_kernel<<<1, kScanBlock, 0, st>>>(d_sums, tiles, d_ctl);
-  NQX_CUDA(cudaGetLastError());
-  add_tile_offsets_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, count, d_sums);
-  NQX_CUDA(cudaGetLastError());
-  unsigned long long h[2];
-  NQX_CUDA(cudaMemcpyAsync(h, d_ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+  DevBuf ctl{nullptr, st};
+  NQX_CUDA(cudaMallocAsync(&ctl.p, 3 * sizeof(unsigned long long), st));
+  auto* d_ctl = static_cast<unsigned long long*>(ctl.p);  // [0] total, [1] bad root, [2] min placed
+  NQX_CUDA(cudaMemsetAsync(d_ctl, 0x00, sizeof(unsigned long long), st));
+  NQX_CUDA(cudaMemsetAsync(d_ctl + 1, 0xff, 2 * sizeof(unsigned long long), st));
+  const uint4* cur = reinterpret_cast<const uint4*>(dev_roots);
+  uint64_t cur_n = count;
+  uint4* owned = nullptr;  // the current level's buffer when we allocated it
+  int passes = -1;         // known after the first count pass
+  for (int pass = 0;; ++pass) {
+    const uint64_t tiles = (cur_n + kScanBlock - 1) / kScanBlock;
+    DevBuf counts{nullptr, st}, sums{nullptr, st};
+    NQX_CUDA(cudaMallocAsync(&counts.p, cur_n * sizeof(unsigned long long), st));
+    NQX_CUDA(cudaMallocAsync(&sums.p, tiles * sizeof(unsigned long long), st));
+    auto* d_counts = static_cast<unsigned long long*>(counts.p);
+    auto* d_sums = static_cast<unsigned long long*>(sums.p);
+    const int threads = 256;
+    const int grid = static_cast<int>(std::min<uint64_t>((cur_n + threads - 1) / threads,
+                                                         static_cast<uint64_t>(sms) * 32));
+    level_count_kernel<<<grid, threads, 0, st>>>(cur, cur_n, mask, target, d_counts,
+                                                 pass == 0 ? d_ctl + 1 : nullptr,
+                                                 reinterpret_cast<unsigned int*>(d_ctl + 2));
+    NQX_CUDA(cudaGetLastError());
+    scan_tiles_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, cur_n, d_sums);
+    scan_sums_kernel<<<1, kScanBlock, 0, st>>>(d_sums, tiles, d_ctl);
+    add_tile_offsets_kernel<<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_counts, cur_n, d_sums);
+    NQX_CUDA(cudaGetLastError());
+    unsigned long long h[3];
+    NQX_CUDA(cudaMemcpyAsync(h, d_ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+    NQX_CUDA(cudaStreamSynchronize(st));
+    if (pass == 0) {
+      if (h[1] != ~0ull) return set_error(NQ_ECONFIG, "root " + std::to_string(h[1]) + " is malformed");
+      const int min_placed = static_cast<int>(h[2] & 0xffffffffu);
+      passes = std::max(target - min_placed, 1);  // >= 1 pass: the output is a fresh buffer
+    }
+    uint4* next = nullptr;
+    NQX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&next), std::max<uint64_t>(h[0], 1) * 16, st));
+    level_emit_kernel<<<grid, threads, 0, st>>>(cur, cur_n, mask, target, d_counts, next);
+    NQX_CUDA(cudaGetLastError());
+    if (owned) NQX_CUDA(cudaFreeAsync(owned, st));
+    owned = next;
+    cur = next;
+    cur_n = h[0];
+    if (pass + 1 >= passes) break;
+  }
   NQX_CUDA(cudaStreamSynchronize(st));
-  if (h[1] != ~0ull)
-    return set_error(NQ_ECONFIG, "root " + std::to_string(h[1]) +
-                                     " is malformed or more than " +
-                                     std::to_string(kExpandMaxDepth) + " rows from the target");
-  *total = h[0];
-  if (!dev_out || cap == 0) return NQ_OK;
-  if (h[0] > cap)
+  *out = owned;
+  *total = cur_n;
+  return NQ_OK;
+}
+
+}  // namespace nqb200
+
+extern "C" int nq_expand_device(int device, int n, const nq_sub* dev_roots, uint64_t count,
+                                int target_rows, nq_sub* dev_out, uint64_t cap, uint64_t* total) {
+  if (!total) return set_error(NQ_ECONFIG, "null total");
+  *total = 0;
+  const cudaStream_t st = cudaStreamPerThread;  // no implicit sync with other workers' streams
+  uint4* buf = nullptr;
+  uint64_t n_out = 0;
+  if (int rc = expand_levels(device, n, dev_roots, count, target_rows, st, &buf, &n_out)) {
+    if (buf) cudaFreeAsync(buf, st);
+    return rc;
+  }
+  DevBuf guard{buf, st};
+  *total = n_out;
+  if (!dev_out || cap == 0 || n_out == 0) return NQ_OK;
+  if (n_out > cap)
     return set_error(NQ_ECONFIG, "output capacity " + std::to_string(cap) + " below the " +
-                                     std::to_string(h[0]) + " deepened records");
-  expand_emit_kernel<<<grid, threads, 0, st>>>(roots, count, mask, target_rows, d_counts, dev_out, h[0]);
-  NQX_CUDA(cudaGetLastError());
+                                     std::to_string(n_out) + " deepened records");
+  NQX_CUDA(cudaMemcpyAsync(dev_out, buf, n_out * sizeof(nq_sub), cudaMemcpyDeviceToDevice, st));
   NQX_CUDA(cudaStreamSynchronize(st));
   return NQ_OK;
 }
