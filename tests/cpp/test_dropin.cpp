@@ -224,6 +224,7 @@ void frontier_cases() {  // test_subproblems.cpp:34-150
   for (int n : {5, 8, 9, 12})
     for (int r = 1; r <= 4 && r < n; ++r) CHECK(count_subproblems(n, r) == generate({n, r}).size());
   CHECK(count_subproblems(27, 7) == 453688251ull);  // acceptance.cpp:77-89
+  CHECK(kQueens27Reference == 234907967154122528ull);  // acceptance.cpp:234-239
 
   std::uint64_t streamed = 0;
   for_each_subproblem({12, 4}, [&](const Subproblem&) { ++streamed; });

@@ -45,3 +45,25 @@ def test_resume_of_bad_checkpoint_exits_4(tmp_path):
     p.write_text("nqb200-checkpoint 1\nchecksum 0\n")
     assert run("resume", str(p)).returncode == 4
     assert run("solve", "--n", "12", "--checkpoint", str(p), "--resume").returncode == 4
+
+
+def test_criterion_9_q27_reference_constant():
+    """acceptance.cpp:234-239: the 27-queens total is kept as a named constant."""
+    from paper_2511_12009_b200 import nqueens as nq
+    assert nq.kQueens27Reference == 234907967154122528
+
+
+@pytest.mark.gpu
+def test_criterion_10_growth_ratio_via_bench():
+    """acceptance.cpp:241-285: `bench` reports Q(n)/Q(n-1) > 1 for n = 10..15."""
+    out = run("bench", "--n-min", "9", "--n-max", "15", "--r-min", "2", "--r-max", "2", "--reps", "1")
+    assert out.returncode == 0
+    lines = out.stdout.strip().splitlines()
+    assert lines[0] == "n,r,config,kernel,reps,median_ms,total,ratio"
+    rows = [l.split(",") for l in lines[1:]]
+    assert len(rows) == 7
+    for i, cells in enumerate(rows):
+        assert len(cells) == 8
+        if i:
+            assert float(cells[7]) > 1.0
+    assert [int(c[6]) for c in rows] == [352, 724, 2680, 14200, 73712, 365596, 2279184]
