@@ -403,3 +403,14 @@ def test_context_refuses_a_second_launch_while_one_is_in_flight(oracle):
     assert r.solutions == 14772512
     assert c.count(16, 5, a).solutions == 14772512
     c.close()
+
+
+def test_report_json_consistent_totals():
+    """test_scheduler.cpp:149-163: the report serialises with per-worker partial sums
+    that add up to the total."""
+    opts = nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.weighted, 4, [0.4, 0.3, 0.2, 0.1]))
+    rep = nq.execute(10, 2, opts)
+    j = rep.to_json()
+    assert j["n"] == 10 and j["total"] == rep.total == 724
+    assert len(j["workers"]) == 4 and j["partition"] == "weighted"
+    assert sum(w["partial_sum"] for w in j["workers"]) == rep.total
