@@ -89,6 +89,11 @@ int nq_ctx_set_tuning(nq_ctx* ctx, int block, int blocks_per_sm, int reverse_ord
 #define NQ_LAYOUT_V4 0
 #define NQ_LAYOUT_PLANES 1
 int nq_ctx_set_layout(nq_ctx* ctx, int layout);
+/* Tail balancing (default on): once the dispatch queue is empty, an idle lane takes the
+ * shallowest pending frame of a busy lane in its warp (the largest remaining subtree),
+ * so one skewed subproblem no longer leaves 31 lanes idle. Totals are unchanged; off
+ * only for A/B measurements. (count_each never splits a record.) */
+int nq_ctx_set_balance(nq_ctx* ctx, int donate);
 /* Host cancel flag (may be NULL) polled while a synchronous call waits: once it reads
  * non-zero, the running kernel stops handing out records at its next refill (lanes
  * finish the subtree they hold), and the call returns with result.subproblems below the

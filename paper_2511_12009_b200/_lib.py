@@ -109,6 +109,7 @@ _sigs = {
     "nq_ctx_set_tuning": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "nq_ctx_set_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "nq_ctx_set_cancel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "nq_ctx_set_balance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "nq_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_void_p, _u64, _P(NqResult)]),
     "nq_count_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -111,6 +111,7 @@ struct nq_ctx {
   int blocks_per_sm = 0;                   // 0 = occupancy limit
   int reverse = 1;
   int layout = NQ_LAYOUT_V4;
+  int donate = 1;                          // intra-warp tail balancing
   // in-flight batch (nq_count_device_async / nq_collect)
   bool pending = false;
   int p_variant = 1;
@@ -207,6 +208,7 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.min_placed = pre_rows;
   P.reverse = c->reverse;
   P.lastrow = variant == NQ_VARIANT_LASTROW;
+  P.donate = c->donate;
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
   if (count > 0) {
     L.fn<<<L.grid, c->block, L.smem, c->stream>>>(P);
@@ -340,6 +342,12 @@ int nq_ctx_set_tuning(nq_ctx* c, int block, int blocks_per_sm, int reverse_order
 int nq_ctx_set_cancel(nq_ctx* c, const volatile int* cancel) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
   c->cancel = cancel;
+  return NQ_OK;
+}
+
+int nq_ctx_set_balance(nq_ctx* c, int donate) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  c->donate = donate ? 1 : 0;
   return NQ_OK;
 }
 

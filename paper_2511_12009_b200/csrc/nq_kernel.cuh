@@ -50,6 +50,7 @@ struct DfsParams {
   int min_placed;                    // batch pre_rows: deeper records would overflow the stack
   int reverse;                       // dispatch order: 1 = last record first
   int lastrow;                       // variant (affects high-water / node outputs only)
+  int donate;                        // tail balancing: idle lanes take busy lanes' frames
 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
@@ -91,6 +92,32 @@ __device__ __forceinline__ void lds128(uint32_t addr, uint32_t& x, uint32_t& y, 
 //                 at four memory instructions per push / pop (~5% slower, dfs_lab).
 constexpr int kLayoutV4 = 0;
 constexpr int kLayoutPlanes = 1;
+
+// One whole frame at a stack address of the given layout (the donation path).
+template <uint32_t STRIDE, int LAYOUT>
+__device__ __forceinline__ void load_frame(uint32_t addr, uint32_t& C, uint32_t& l, uint32_t& r,
+                                           uint32_t& a) {
+  if constexpr (LAYOUT == kLayoutV4) {
+    lds128(addr, C, l, r, a);
+  } else {
+    asm volatile("ld.shared.u32 %0, [%4];\n\tld.shared.u32 %1, [%4+%5];\n\t"
+                 "ld.shared.u32 %2, [%4+%6];\n\tld.shared.u32 %3, [%4+%7];"
+                 : "=r"(C), "=r"(l), "=r"(r), "=r"(a)
+                 : "r"(addr), "n"(STRIDE / 4), "n"(STRIDE / 2), "n"(3 * STRIDE / 4)
+                 : "memory");
+  }
+}
+
+template <uint32_t STRIDE, int LAYOUT>
+__device__ __forceinline__ void store_idle_frame(uint32_t addr) {
+  if constexpr (LAYOUT == kLayoutV4) {
+    sts128(addr, 0u, 0u, 0u, 0u);
+  } else {
+#pragma unroll
+    for (uint32_t w = 0; w < 4; ++w)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr + w * (STRIDE / 4)), "r"(0u) : "memory");
+  }
+}
 
 template <uint32_t STRIDE, int LAYOUT>
 __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
@@ -182,6 +209,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
 
   uint32_t C = kIdleC, l = 0u, r = 0u, a = 0u;  // current row state (idle)
   uint32_t sp = base1;                             // next free frame
+  uint32_t bp = base1;                             // lowest frame not yet given away
+  bool piece = false;                              // the lane holds a donated frame
   uint32_t sol = 0u, its = 0u;                     // per-lane counters since last fold
   uint32_t weight = 0u;                            // multiplier of the current record
   bool busy = false;                               // lane holds a record
@@ -198,11 +227,12 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
     uint32_t idle = __ballot_sync(0xffffffffu, a == 0u);
     if (idle) {
       for (;;) {
-        if (a == 0u && busy) {  // fold the finished record
+        if (a == 0u && busy) {  // fold the finished record (or donated piece of one)
           tot_w += static_cast<unsigned long long>(weight) * sol;
           tot_raw += sol;
           tot_it += its;
-          tot_subs += 1ull;
+          tot_subs += piece ? 0ull : 1ull;
+          piece = false;
           if constexpr (PER_SUB) {
             sub_sol += sol;
             sub_it += its;
@@ -255,8 +285,50 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
               r = s.z;
               a = C & ~(l | r);  // valid_positions (bitboard.hpp:21-23)
               sp = base1;
+              bp = base1;
             }
             if (a == 0u) C = kIdleC;  // settled at the root: back to the idle state
+          }
+        }
+      }
+      if constexpr (!PER_SUB) {
+        // Tail balancing inside the warp. Once the queue is empty, an idle lane takes
+        // the SHALLOWEST pending frame of a busy lane — the row with untried candidates
+        // nearest the root, i.e. the largest remaining subtree — and the donor marks that
+        // slot idle, so popping down to it later ends the donor's work there. Frames never
+        // move: a lane's live frames are [bp, sp); everything below bp was given away.
+        if (exhausted && P.donate) {
+          for (int round = 0; round < 2; ++round) {
+            const uint32_t idle_m = __ballot_sync(0xffffffffu, a == 0u);
+            const uint32_t donor_m = __ballot_sync(0xffffffffu, a != 0u && sp > bp);
+            if (idle_m == 0u || donor_m == 0u) break;
+            const uint32_t lt = (1u << lane) - 1u;
+            const uint32_t k = min(__popc(idle_m), __popc(donor_m));
+            const uint32_t my_idle = __popc(idle_m & lt), my_donor = __popc(donor_m & lt);
+            const bool recv = a == 0u && my_idle < k;
+            const bool give = ((donor_m >> lane) & 1u) && my_donor < k;
+            uint32_t src = lane;
+            if (recv) {  // the my_idle-th donor
+              uint32_t m = donor_m;
+              for (uint32_t i = 0; i < my_idle; ++i) m &= m - 1u;
+              src = __ffs(m) - 1u;
+            }
+            const uint32_t d_bp = __shfl_sync(0xffffffffu, bp, src);
+            const uint32_t d_w = __shfl_sync(0xffffffffu, weight, src);
+            if (recv) {
+              load_frame<STRIDE, LAYOUT>(d_bp, C, l, r, a);
+              weight = d_w;
+              sp = base1;
+              bp = base1;
+              busy = true;
+              piece = true;
+            }
+            __syncwarp();
+            if (give) {
+              store_idle_frame<STRIDE, LAYOUT>(bp);
+              bp += STRIDE;
+            }
+            __syncwarp();
           }
         }
       }

@@ -133,3 +133,23 @@ def test_execute_rejects_bad_options_before_device_work():
         nq.execute_batch(8, 2, nq.generate_packed(8, 2), opts)
     with pytest.raises(nq.ConfigError):
         nq.partition_strategy_from("roundrobin")
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/nq_gpu.h compiles as strict C99 and a C program links libnqb200.so —
+    the boundary a cgo / JNI / ctypes binding sees."""
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "c_abi.c"
+    src.write_text('#include "nq_gpu.h"\n'
+                   "int main(void) { nq_result r; nq_solve_opts o = {0}; uint64_t t = 0;\n"
+                   "  (void)r; (void)o;\n"
+                   "  if (nq_count_subproblems(27, 7, &t) != NQ_OK || t != 453688251ull) return 2;\n"
+                   "  if (nq_count_subproblems(5, 9, &t) != NQ_ECONFIG) return 3;\n"
+                   "  return nq_abi_version() == NQ_ABI_VERSION ? 0 : 4; }\n")
+    exe = tmp_path / "c_abi"
+    lib_dir = os.path.join(repo, "paper_2511_12009_b200")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                    "-I" + os.path.join(repo, "include"), str(src), "-L" + lib_dir, "-l:libnqb200.so",
+                    "-Wl,-rpath," + lib_dir, "-o", str(exe)], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0

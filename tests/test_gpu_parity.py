@@ -23,10 +23,11 @@ def as_recs(lst):
 
 
 class Ctx:
-    def __init__(self, block=0, bps=0, reverse=1, layout=_lib.LAYOUT_V4):
+    def __init__(self, block=0, bps=0, reverse=1, layout=_lib.LAYOUT_V4, balance=1):
         self.p = ctypes.c_void_p()
         _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(self.p)))
         _lib.check(_lib.lib.nq_ctx_set_layout(self.p, layout))
+        _lib.check(_lib.lib.nq_ctx_set_balance(self.p, balance))
         _lib.check(_lib.lib.nq_ctx_set_tuning(self.p, block, bps, reverse))
 
     def count(self, n, pre_rows, a, variant=_lib.VARIANT_LASTROW):
@@ -163,16 +164,16 @@ def test_cancel_before_start():
 def test_tuning_variants_identical(oracle):
     a = oracle.generate(15, 5)
     base = None
-    for layout in (_lib.LAYOUT_V4, _lib.LAYOUT_PLANES):
+    for layout, balance in ((_lib.LAYOUT_V4, 1), (_lib.LAYOUT_V4, 0), (_lib.LAYOUT_PLANES, 1)):
         for block in (64, 96, 128, 192, 256):
             for reverse in (0, 1):
                 for bps in (0, 1):
-                    c = Ctx(block, bps, reverse, layout)
+                    c = Ctx(block, bps, reverse, layout, balance)
                     r = c.count(15, 5, a)
                     c.close()
                     got = (r.solutions, r.raw_solutions, r.nodes, r.subproblems)
                     base = base or got
-                    assert got == base, (layout, block, reverse, bps)
+                    assert got == base, (layout, balance, block, reverse, bps)
     assert base[0] == 2279184 and base[3] == len(a)
 
 
@@ -414,3 +415,24 @@ def test_report_json_consistent_totals():
     assert j["n"] == 10 and j["total"] == rep.total == 724
     assert len(j["workers"]) == 4 and j["partition"] == "weighted"
     assert sum(w["partial_sum"] for w in j["workers"]) == rep.total
+
+
+def test_tail_donation_keeps_every_count_and_balances(golden):
+    """Intra-warp donation splits subtrees between lanes at the end of a launch: the
+    weighted total, raw total, node count and record count are unchanged — on a
+    maximally skewed input (N=18 from R=3: 36 huge subtrees for ~150k lanes, so
+    nearly all the work is donated) and on a full frontier."""
+    for n, r in ((18, 3), (17, 6)):
+        recs = nq.generate_packed(n, r)
+        outs = []
+        for balance in (0, 1):
+            c = Ctx(balance=balance)
+            res = c.count(n, r, recs)
+            c.close()
+            outs.append((res.solutions, res.raw_solutions, res.nodes, res.subproblems, res.kernel_ms))
+        assert outs[0][:4] == outs[1][:4], outs
+        assert outs[1][0] == golden["oeis_a000170"][n - 1]
+        if r == 3:  # a from-the-root split: Alg. 3 nodes from R=3 = R=5 count + rows 4, 5
+            want = golden["appendix_b_nodes"]["18"]["5"] + nq.count_subproblems(18, 4) + nq.count_subproblems(18, 5)
+            assert outs[1][2] == want
+            assert outs[1][4] < outs[0][4], outs  # donation must help when work is this skewed

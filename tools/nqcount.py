@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="blocks x blocks-per-SM sweep")
     ap.add_argument("--variant", type=int, default=1)
     ap.add_argument("--layout", type=int, default=0, help="0 = uint4 frames, 1 = 32-bit planes")
+    ap.add_argument("--balance", type=int, default=1, help="1 = intra-warp tail donation")
     args = ap.parse_args()
 
     import numpy as np
@@ -47,6 +48,7 @@ def main():
     ctx = ctypes.c_void_p()
     _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(ctx)))
     _lib.check(_lib.lib.nq_ctx_set_layout(ctx, args.layout))
+    _lib.check(_lib.lib.nq_ctx_set_balance(ctx, args.balance))
     configs = [(args.block, args.bps)]
     if args.sweep:
         configs = [(b, k) for b in (64, 96, 128, 192, 256) for k in (0,)]
@@ -63,7 +65,7 @@ def main():
         ok = args.n > len(OEIS) or best.solutions == OEIS[args.n - 1]
         rate = best.nodes / (best.kernel_ms * 1e-3)
         print(json.dumps({"n": args.n, "pre_rows": args.pre_rows, "block": block or 128,
-                          "bps": bps, "order": args.order, "layout": args.layout, "records": len(subs),
+                          "bps": bps, "order": args.order, "layout": args.layout, "balance": args.balance, "records": len(subs),
                           "solutions": best.solutions, "ok": ok, "nodes": best.nodes,
                           "iterations": best.iterations, "kernel_ms": round(best.kernel_ms, 3),
                           "nodes_per_s": rate,

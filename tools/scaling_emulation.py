@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--pre-rows", type=int, default=7)
     ap.add_argument("--ks", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--balance", type=int, default=1)
     args = ap.parse_args()
 
     import numpy as np
@@ -36,6 +37,7 @@ def main():
 
     ctx = ctypes.c_void_p()
     _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(ctx)))
+    _lib.check(_lib.lib.nq_ctx_set_balance(ctx, args.balance))
     t1 = None
     rows = []
     for k in [int(x) for x in args.ks.split(",")]:
@@ -57,7 +59,7 @@ def main():
         tk = max(times)
         if k == 1:
             t1 = tk
-        row = {"k": k, "per_rank_ms": [round(t, 3) for t in times], "T_k_ms": round(tk, 3),
+        row = {"k": k, "balance": args.balance, "per_rank_ms": [round(t, 3) for t in times], "T_k_ms": round(tk, 3),
                "rank_spread": round(max(times) / min(times), 4), "solutions": sols, "nodes": nodes,
                "nodes_per_s_k_gpus": nodes / (tk * 1e-3),
                "efficiency": (t1 / (k * tk)) if t1 else None}
