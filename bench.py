@@ -231,10 +231,10 @@ def main():
         # R=7: 22.8 M finer subtrees keep every lane busy to the end (lane efficiency
         # 99.7% vs 97.9% at R=6, tools/microbench/dfs_lab.cu) and the shallower stack
         # fits one more block per SM.
-        # With 4+ ranks each GPU holds 1/k of the frontier; R=8 keeps ~150 records per
-        # lane so the per-GPU tail stays short (tools/scaling_emulation.py: 8-way
-        # efficiency 95.1% at R=7, 99.1% at R=8; one GPU is equally fast at both).
-        args.pre_rows = (8 if world >= 4 else 7) if args.n >= 19 else 6
+        # R=7 at every world size: with the kernel's tail donation the slowest of 8
+        # stratified shards runs at 99.4% of ideal (tools/scaling_emulation.py; 95.4%
+        # without donation), and the shard is 8x smaller to ship than at R=8.
+        args.pre_rows = 7 if args.n >= 19 else 6
     if args.impl == "reference":
         return run_reference_arm(args)
 
