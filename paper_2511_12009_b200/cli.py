@@ -61,8 +61,12 @@ def do_solve(nq, a):
     if a.checkpoint:
         cancel = _sigint_event()
         opts.cancel = cancel
-        rep = nq.execute_checkpointed(a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
-                                      flush_interval_s=a.checkpoint_interval_s, resume=a.resume)
+        if getattr(a, "time_limit_s", 0):
+            import threading
+            threading.Timer(a.time_limit_s, cancel.set).start()
+        rep = _run_interruptible(lambda: nq.execute_checkpointed(
+            a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
+            flush_interval_s=a.checkpoint_interval_s, resume=a.resume), cancel)
         if rep.completed:
             log(nq.log_result_line(a.n, rep.total, rep.calc_ms))
         else:
@@ -77,6 +81,27 @@ def do_solve(nq, a):
             print(f"{w.worker},{w.assigned},{w.processed},{w.partial_sum},{w.elapsed_ms}")
         print(f"total,,,{rep.total},{rep.calc_ms}")
     return EXIT_OK
+
+
+def _run_interruptible(fn, cancel):
+    """Runs fn in a worker thread so the main thread keeps handling SIGINT/SIGTERM (a
+    Python signal handler cannot run while the main thread is inside a C call)."""
+    import threading
+    box = {}
+
+    def work():
+        try:
+            box["r"] = fn()
+        except BaseException as e:  # noqa: BLE001 — re-raised in the main thread
+            box["e"] = e
+
+    t = threading.Thread(target=work, daemon=True)
+    t.start()
+    while t.is_alive():
+        t.join(0.2)
+    if "e" in box:
+        raise box["e"]
+    return box["r"]
 
 
 def _sigint_event():
@@ -159,10 +184,13 @@ def main(argv=None):
     s.add_argument("--checkpoint-chunk", type=int, default=0, help="records per chunk (0 = auto)")
     s.add_argument("--checkpoint-interval-s", type=float, default=30.0,
                    help="rewrite the checkpoint at most this often")
+    s.add_argument("--time-limit-s", type=float, default=0.0,
+                   help="checkpointed runs: cancel (and save progress) after this many seconds")
     rs = sub.add_parser("resume", help="continue an interrupted checkpointed run")
     rs.add_argument("checkpoint")
     rs.add_argument("--format", default="log", choices=["json", "csv", "log"])
     rs.add_argument("--checkpoint-interval-s", type=float, default=30.0)
+    rs.add_argument("--time-limit-s", type=float, default=0.0)
     for k, v in (("config", "config2"), ("workers", None), ("partition", "stealing"),
                  ("weights", ""), ("kernel", "lastrow"), ("chunk_size", 4096),
                  ("export_subproblems", ""), ("gpus", 0), ("devices", "")):
