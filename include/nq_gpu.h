@@ -226,6 +226,8 @@ typedef struct nq_ckpt_opts {
   uint64_t chunk;            /* records per chunk; 0 = ceil(tasks / 256) (or the file's)  */
   double flush_interval_s;   /* rewrite at most this often; 0 = after every chunk         */
   int resume;                /* 1 = continue the run recorded in path                     */
+  double stop_after_s;       /* >0: start no new chunk after this many seconds (the       */
+                             /* running ones finish and are recorded); 0 = no limit      */
 } nq_ckpt_opts;
 
 /* execute() with chunk-granular progress: the folded frontier is cut into fixed chunks;

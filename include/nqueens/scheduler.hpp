@@ -380,7 +380,7 @@ inline SolveReport execute_checkpointed(int n, int pre_rows, const ExecuteOption
     o.stack_depth = opts.config.max_depth();
     const std::string cfg_name(opts.config.name);
     o.config_name = cfg_name.c_str();
-    nq_ckpt_opts ck{path.c_str(), chunk, flush_interval_s, resume ? 1 : 0};
+    nq_ckpt_opts ck{path.c_str(), chunk, flush_interval_s, resume ? 1 : 0, 0.0};
     nq_report rep{};
     gpu::check(nq_solve_checkpointed(n, pre_rows, &o, &ck, &rep));
     SolveReport report;

@@ -73,7 +73,8 @@ class NqReport(ctypes.Structure):
 
 class NqCkptOpts(ctypes.Structure):
     _fields_ = [("path", ctypes.c_char_p), ("chunk", ctypes.c_uint64),
-                ("flush_interval_s", ctypes.c_double), ("resume", ctypes.c_int)]
+                ("flush_interval_s", ctypes.c_double), ("resume", ctypes.c_int),
+                ("stop_after_s", ctypes.c_double)]
 
 
 PARTITION_UNIFORM, PARTITION_WEIGHTED, PARTITION_STEALING, PARTITION_GUIDED, PARTITION_STRIDED = 0, 1, 2, 3, 4

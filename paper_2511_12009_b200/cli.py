@@ -66,7 +66,8 @@ def do_solve(nq, a):
             threading.Timer(a.time_limit_s, cancel.set).start()
         rep = _run_interruptible(lambda: nq.execute_checkpointed(
             a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
-            flush_interval_s=a.checkpoint_interval_s, resume=a.resume), cancel)
+            flush_interval_s=a.checkpoint_interval_s, resume=a.resume,
+            stop_after_s=getattr(a, "stop_after_s", 0.0)), cancel)
         if rep.completed:
             log(nq.log_result_line(a.n, rep.total, rep.calc_ms))
         else:
@@ -186,11 +187,14 @@ def main(argv=None):
                    help="rewrite the checkpoint at most this often")
     s.add_argument("--time-limit-s", type=float, default=0.0,
                    help="checkpointed runs: cancel (and save progress) after this many seconds")
+    s.add_argument("--stop-after-s", type=float, default=0.0,
+                   help="checkpointed runs: start no new chunk after this many seconds")
     rs = sub.add_parser("resume", help="continue an interrupted checkpointed run")
     rs.add_argument("checkpoint")
     rs.add_argument("--format", default="log", choices=["json", "csv", "log"])
     rs.add_argument("--checkpoint-interval-s", type=float, default=30.0)
     rs.add_argument("--time-limit-s", type=float, default=0.0)
+    rs.add_argument("--stop-after-s", type=float, default=0.0)
     for k, v in (("config", "config2"), ("workers", None), ("partition", "stealing"),
                  ("weights", ""), ("kernel", "lastrow"), ("chunk_size", 4096),
                  ("export_subproblems", ""), ("gpus", 0), ("devices", "")):

@@ -258,6 +258,11 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
           interrupted.store(true);
           break;
         }
+        if (ck->stop_after_s > 0 &&
+            std::chrono::duration<double>(clk::now() - t0).count() >= ck->stop_after_s) {
+          interrupted.store(true);  // soft deadline: leave the rest for a resumed run
+          break;
+        }
         const size_t k = cursor.fetch_add(1);
         if (k >= pending.size()) break;
         const uint64_t ci = pending[k];

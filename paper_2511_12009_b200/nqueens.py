@@ -595,7 +595,8 @@ def execute(n: int, pre_rows: int, opts: ExecuteOptions) -> SolveReport:
 
 
 def execute_checkpointed(n: int, pre_rows: int, opts: ExecuteOptions, path: str, chunk: int = 0,
-                         flush_interval_s: float = 0.0, resume: bool = False) -> SolveReport:
+                         flush_interval_s: float = 0.0, resume: bool = False,
+                         stop_after_s: float = 0.0) -> SolveReport:
     """execute() with chunk-granular checkpoint/resume (nq_solve_checkpointed; the GPU
     counterpart of run_with_checkpoint, runner.hpp:48-212). Workers take pending chunks;
     a cancel leaves completed = False and a file a later resume=True call continues."""
@@ -607,7 +608,8 @@ def execute_checkpointed(n: int, pre_rows: int, opts: ExecuteOptions, path: str,
                             log=opts.log, cancel=opts.cancel, devices=opts.devices)
     keep: list = []
     o = _solve_opts(o_opts, keep)
-    ck = _lib.NqCkptOpts(str(path).encode(), chunk, flush_interval_s, 1 if resume else 0)
+    ck = _lib.NqCkptOpts(str(path).encode(), chunk, flush_interval_s, 1 if resume else 0,
+                         stop_after_s)
     rep = _lib.NqReport()
     try:
         _call(lib.nq_solve_checkpointed(n, pre_rows, ctypes.byref(o), ctypes.byref(ck), ctypes.byref(rep)))
