@@ -121,3 +121,17 @@ def test_run_with_checkpoint_round_trip(tmp_path):
     assert any("n 15 queens result 2279184" in l for l in lines)
     assert nq.run_with_checkpoint(spec, nq.CheckpointOptions(p, 5000, resume=True)).total == 2279184
     assert nq.run_with_checkpoint(nq.RunSpec(1, 0), nq.CheckpointOptions(p)).total == 1
+
+
+@pytest.mark.gpu
+def test_soft_stop_records_every_started_chunk(tmp_path):
+    """stop_after_s: no chunk starts after the deadline, the running ones finish and are
+    recorded (nothing discarded); resuming completes the count."""
+    p = tmp_path / "soft.ckpt"
+    first = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, stop_after_s=1e-6)
+    assert not first.completed
+    n, r, chunks, done = nq.checkpoint_info(p)
+    assert 1 <= done < chunks          # the chunk already started when the deadline passed
+    assert sum(w.processed for w in first.workers) == done * 100000 or done == chunks
+    rest = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, resume=True)
+    assert rest.completed and rest.total == 4968057848
