@@ -128,10 +128,10 @@ def test_soft_stop_records_every_started_chunk(tmp_path):
     """stop_after_s: no chunk starts after the deadline, the running ones finish and are
     recorded (nothing discarded); resuming completes the count."""
     p = tmp_path / "soft.ckpt"
-    first = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, stop_after_s=1e-6)
-    assert not first.completed
+    first = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, stop_after_s=0.02)
     n, r, chunks, done = nq.checkpoint_info(p)
-    assert 1 <= done < chunks          # the chunk already started when the deadline passed
-    assert sum(w.processed for w in first.workers) == done * 100000 or done == chunks
+    assert not first.completed and done < chunks
+    # every chunk that started was finished and recorded — none discarded
+    assert sum(w.processed for w in first.workers) == done * 100000
     rest = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, resume=True)
     assert rest.completed and rest.total == 4968057848
