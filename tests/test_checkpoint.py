@@ -131,7 +131,10 @@ def test_soft_stop_records_every_started_chunk(tmp_path):
     first = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, stop_after_s=0.02)
     n, r, chunks, done = nq.checkpoint_info(p)
     assert not first.completed and done < chunks
-    # every chunk that started was finished and recorded — none discarded
-    assert sum(w.processed for w in first.workers) == done * 100000
+    # every chunk that started was finished and recorded — none discarded (chunks go
+    # expensive end first, so the recorded ones are the `done` highest indices)
+    tasks = nq.count_subproblems(19, 6)
+    sizes = [min(100000, tasks - c * 100000) for c in range(chunks)]
+    assert sum(w.processed for w in first.workers) == sum(sizes[chunks - done:])
     rest = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, resume=True)
     assert rest.completed and rest.total == 4968057848
