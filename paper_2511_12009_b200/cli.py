@@ -61,13 +61,21 @@ def do_solve(nq, a):
     if a.checkpoint:
         cancel = _sigint_event()
         opts.cancel = cancel
+        timer = None
         if getattr(a, "time_limit_s", 0):
             import threading
-            threading.Timer(a.time_limit_s, cancel.set).start()
-        rep = _run_interruptible(lambda: nq.execute_checkpointed(
-            a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
-            flush_interval_s=a.checkpoint_interval_s, resume=a.resume,
-            stop_after_s=getattr(a, "stop_after_s", 0.0)), cancel)
+            # Daemon + cancelled on return: a finished run must not wait for the limit.
+            timer = threading.Timer(a.time_limit_s, cancel.set)
+            timer.daemon = True
+            timer.start()
+        try:
+            rep = _run_interruptible(lambda: nq.execute_checkpointed(
+                a.n, pre, opts, a.checkpoint, chunk=a.checkpoint_chunk,
+                flush_interval_s=a.checkpoint_interval_s, resume=a.resume,
+                stop_after_s=getattr(a, "stop_after_s", 0.0)), cancel)
+        finally:
+            if timer is not None:
+                timer.cancel()
         if rep.completed:
             log(nq.log_result_line(a.n, rep.total, rep.calc_ms))
         else:
