@@ -40,6 +40,19 @@ def test_solve_log_and_json():
     assert js.returncode == 0 and '"total": 2680' in js.stdout
 
 
+@pytest.mark.gpu
+def test_time_limit_does_not_delay_a_finished_run(tmp_path):
+    """A checkpointed solve that finishes well inside --time-limit-s exits at once (the
+    limit timer is a daemon and is cancelled on return), with the completed total."""
+    import time
+    t0 = time.monotonic()
+    out = run("solve", "--n", "14", "--pre-rows", "4", "--checkpoint", str(tmp_path / "q14.ckpt"),
+              "--time-limit-s", "240", "--format", "json")
+    assert out.returncode == 0, out.stderr
+    assert '"total": 365596' in out.stdout and '"completed": true' in out.stdout
+    assert time.monotonic() - t0 < 120
+
+
 def test_resume_of_bad_checkpoint_exits_4(tmp_path):
     p = tmp_path / "bad.ckpt"
     p.write_text("nqb200-checkpoint 1\nchecksum 0\n")
