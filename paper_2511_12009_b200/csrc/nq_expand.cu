@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdint>
 #include <string>
 
@@ -157,6 +158,27 @@ namespace {
                                      __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
   } while (0)
 
+// The level buffers (N=20 R=4->7: ~1 GB across passes) come from the device's default
+// stream-ordered pool. Its default release threshold of 0 hands every freed byte back to
+// the driver at the next synchronize, so each call re-maps them (~50 ms at N=20). Keep up
+// to kPoolRetainBytes cached across calls instead.
+constexpr uint64_t kPoolRetainBytes = 8ull << 30;
+
+int retain_pool(int device) {
+  static std::once_flag once[64];
+  if (device < 0 || device >= 64) return NQ_OK;
+  int rc = NQ_OK;
+  std::call_once(once[device], [&] {
+    cudaMemPool_t pool;
+    uint64_t thr = kPoolRetainBytes;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (e != cudaSuccess)
+      rc = set_error(NQ_ECUDA, std::string("default mem pool release threshold: ") + cudaGetErrorString(e));
+  });
+  return rc;
+}
+
 struct DevBuf {  // stream-ordered allocation, freed on the same stream
   void* p = nullptr;
   cudaStream_t s = nullptr;
@@ -184,6 +206,7 @@ int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, in
   if (!dev_roots) return set_error(NQ_ECONFIG, "null roots");
   NvtxRange range("nq_expand_device (level passes)");
   NQX_CUDA(cudaSetDevice(device));
+  if (int rc = retain_pool(device)) return rc;
   const uint32_t mask = (1u << n) - 1u;
   int sms = 0;
   NQX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));

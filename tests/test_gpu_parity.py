@@ -358,7 +358,7 @@ def test_wide_boards_n29_to_31_deep_records(oracle):
 
 def test_execute_deepens_large_frontiers_on_the_device(monkeypatch, golden):
     """nq_solve deals a coarse frontier (R-3) to the workers and deepens it on each
-    device once the R-frontier passes NQB_DEVICE_EXPAND_MIN_RECORDS (default 2^26, e.g.
+    device once the R-frontier passes NQB_DEVICE_EXPAND_MIN_RECORDS (default 2^20, e.g.
     N=27 R=7): same total and the same Alg. 3 node count as the host path."""
     monkeypatch.setenv("NQB_DEVICE_EXPAND_MIN_RECORDS", "1000")
     for workers in (1, 3):
