@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         // slot idle, so popping down to it later ends the donor's work there. Frames never
         // move: a lane's live frames are [bp, sp); everything below bp was given away.
         if (exhausted && P.donate) {
+          // Orders the donors' earlier pushes before the receivers' load_frame below
+          // (ballot/shfl synchronise the warp but do not order shared memory).
+          __syncwarp();
           for (int round = 0; round < 2; ++round) {
             const uint32_t idle_m = __ballot_sync(0xffffffffu, a == 0u);
             const uint32_t donor_m = __ballot_sync(0xffffffffu, a != 0u && sp > bp);
