@@ -289,10 +289,9 @@ private:
 
 }  // namespace detail
 
-/// Counts a pre-generated batch on the GPUs (scheduler.hpp:266-389). Every record is
-/// counted exactly once; totals are independent of strategy and worker count.
-inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subproblem>& batch,
-                                 const ExecuteOptions& opts) {
+namespace detail {
+
+inline void check_execute_options(int n, int pre_rows, const ExecuteOptions& opts) {
     const PartitionPlan& plan = opts.plan;
     if (plan.worker_count < 1) throw config_error("worker_count must be >= 1");
     if (plan.strategy == PartitionStrategy::stealing && plan.chunk_size == 0)
@@ -305,11 +304,12 @@ inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subprobl
         throw config_error("resume is not supported by the GPU executor (checkpointing is out of scope)");
     if (plan.worker_count > NQ_MAX_WORKERS)
         throw config_error("worker_count above " + std::to_string(NQ_MAX_WORKERS));
+}
 
-    std::vector<nq_sub> packed;
-    packed.reserve(batch.size());
-    for (const Subproblem& s : batch) packed.push_back(detail::pack(s));
-
+/// The C-ABI options of `opts`; `cfg_name` and `cancel` must outlive the call.
+inline nq_solve_opts make_solve_opts(const ExecuteOptions& opts, const std::string& cfg_name,
+                                     CancelBridge& cancel) {
+    const PartitionPlan& plan = opts.plan;
     nq_solve_opts o{};
     o.variant = opts.kernel == KernelVariant::lastrow ? NQ_VARIANT_LASTROW : NQ_VARIANT_ITERATIVE;
     o.strategy = detail::to_c_strategy(plan.strategy);
@@ -318,18 +318,20 @@ inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subprobl
     o.chunk = plan.chunk_size;
     o.n_devices = static_cast<int>(opts.devices.size());
     o.devices = opts.devices.empty() ? nullptr : opts.devices.data();
-    detail::CancelBridge cancel(opts.cancel);
     o.cancel = cancel.flag();
     o.stack_depth = opts.config.max_depth();
-    const std::string cfg_name(opts.config.name);
     o.config_name = cfg_name.c_str();
     if (opts.log) {
-        o.log = &detail::log_trampoline;
+        o.log = &log_trampoline;
         o.log_user = const_cast<void*>(static_cast<const void*>(&opts.log));
     }
-    nq_report rep{};
-    gpu::check(nq_solve_batch(n, pre_rows, packed.data(), packed.size(), &o, &rep));
+    return o;
+}
 
+inline SolveReport to_report(int n, int pre_rows, const ExecuteOptions& opts,
+                             const std::string& cfg_name, std::uint64_t task_count,
+                             const nq_report& rep) {
+    const PartitionPlan& plan = opts.plan;
     SolveReport report;
     report.n = n;
     report.pre_rows = pre_rows;
@@ -337,7 +339,7 @@ inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subprobl
     report.kernel = opts.kernel;
     report.strategy = plan.strategy;
     report.worker_count = plan.worker_count;
-    report.task_count = batch.size();
+    report.task_count = task_count;
     report.calc_ms = rep.calc_ms;
     report.total = rep.total;
     report.nodes = rep.nodes;
@@ -359,6 +361,24 @@ inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subprobl
             opts.progress->commit(w, WorkerProgress{s.processed, s.partial_sum});
     }
     return report;
+}
+
+}  // namespace detail
+
+/// Counts a pre-generated batch on the GPUs (scheduler.hpp:266-389). Every record is
+/// counted exactly once; totals are independent of strategy and worker count.
+inline SolveReport execute_batch(int n, int pre_rows, const std::vector<Subproblem>& batch,
+                                 const ExecuteOptions& opts) {
+    detail::check_execute_options(n, pre_rows, opts);
+    std::vector<nq_sub> packed;
+    packed.reserve(batch.size());
+    for (const Subproblem& s : batch) packed.push_back(detail::pack(s));
+    const std::string cfg_name(opts.config.name);
+    detail::CancelBridge cancel(opts.cancel);
+    const nq_solve_opts o = detail::make_solve_opts(opts, cfg_name, cancel);
+    nq_report rep{};
+    gpu::check(nq_solve_batch(n, pre_rows, packed.data(), packed.size(), &o, &rep));
+    return detail::to_report(n, pre_rows, opts, cfg_name, batch.size(), rep);
 }
 
 /// execute() with chunk-granular checkpoint / resume (nq_solve_checkpointed): the GPU
@@ -427,6 +447,20 @@ inline SolveReport execute(int n, int pre_rows, const ExecuteOptions& opts) {
         for (int w = 0; w < opts.plan.worker_count; ++w) report.workers[w].worker = w;
         report.workers[0].partial_sum = 1;
         if (opts.log) opts.log(log_result_line(1, 1, 0.0));
+        return report;
+    }
+    if (opts.plan.strategy == PartitionStrategy::strided) {
+        // nq_solve generates the frontier itself and, from 2^20 records up, deals a
+        // coarser one to the workers to be deepened on their devices (no host copy of
+        // the full frontier, no H2D of it). Same totals, nodes and log lines.
+        detail::check_execute_options(n, pre_rows, opts);
+        const std::string cfg_name(opts.config.name);
+        detail::CancelBridge cancel(opts.cancel);
+        const nq_solve_opts o = detail::make_solve_opts(opts, cfg_name, cancel);
+        nq_report rep{};
+        gpu::check(nq_solve(n, pre_rows, &o, &rep));
+        SolveReport report = detail::to_report(n, pre_rows, opts, cfg_name, rep.task_count, rep);
+        report.generation_ms = rep.generation_ms;
         return report;
     }
     const auto t0 = std::chrono::steady_clock::now();

@@ -424,6 +424,37 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   CHECK(one.total == 1 && one.workers.size() == 1);
   CHECK(execute(18, 6, ExecuteOptions{}).total == 666090624ull);
 
+  // strided plans go through nq_solve: N=16 R=7 (1 999 228 records >= 2^20) is dealt as
+  // the R=4 frontier and deepened on the device; N=10 stays on the host frontier.
+  for (int w : {1, 3}) {
+    std::vector<std::string> slines;
+    ExecuteOptions s;
+    s.plan.strategy = PartitionStrategy::strided;
+    s.plan.worker_count = w;
+    s.log = [&](const std::string& l) {
+      std::lock_guard<std::mutex> lk(mu);
+      slines.push_back(l);
+    };
+    const auto srep = execute(16, 7, s);
+    CHECK(srep.completed && srep.total == 14772512ull);
+    CHECK(srep.task_count == count_subproblems(16, 7));
+    CHECK(static_cast<int>(srep.workers.size()) == w);
+    std::uint64_t sp = 0;
+    for (const auto& ws : srep.workers) sp += ws.processed;
+    CHECK(sp == srep.task_count);
+    bool sres = false;
+    for (const auto& l : slines) sres |= l.find("n 16 queens result 14772512, calc time: [") != std::string::npos;
+    CHECK(sres);
+  }
+  {
+    ExecuteOptions s;
+    s.plan.strategy = PartitionStrategy::strided;
+    s.plan.worker_count = 2;
+    CHECK(execute(10, 3, s).total == 724);
+    s.cancel = &stop;
+    CHECK(!execute(16, 7, s).completed);
+  }
+
   // chunk-granular checkpoint round trip (nq_solve_checkpointed)
   const std::string ck = "/tmp/nqb200_dropin_test.ckpt";
   ExecuteOptions two;
