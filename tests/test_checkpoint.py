@@ -43,6 +43,23 @@ def test_completed_checkpoint_resumes_without_a_device(tmp_path):
     assert rep.completed and rep.total == 14200 and rep.nodes == 7 * k
 
 
+def test_committed_n24_checkpoint_holds_q24(tmp_path):
+    """runs/n24.ckpt is the file the four-call N=24 run on a B200 left behind (profiles/
+    README.md). The library's own reader accepts it: the identity matches N=24, R=7, the
+    lastrow kernel and chunk 9 058 722, and the checksum is valid. Resuming it needs no
+    device, and its chunk sums add up to OEIS A000170(24)."""
+    import shutil
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "runs", "n24.ckpt")
+    p = tmp_path / "n24.ckpt"
+    shutil.copy(src, p)
+    assert nq.checkpoint_info(p) == (24, 7, 16, 16)
+    rep = nq.execute_checkpointed(24, 7, nq.ExecuteOptions(config=nq.find_config("config1")), p,
+                                  chunk=9058722, resume=True)
+    assert rep.completed and rep.total == 227514171973736
+    assert rep.task_count == nq.count_subproblems(24, 7) == 144939546
+    assert rep.nodes == 12749488348460170
+
+
 def test_corrupt_and_foreign_checkpoints_are_rejected(tmp_path):
     n, r = 12, 4
     tasks = nq.count_subproblems(n, r)
