@@ -40,7 +40,7 @@ extern "C" {
 #define NQ_ECANCEL (-4)
 #define NQ_ECHECKPOINT (-5)
 
-#define NQ_ABI_VERSION 1
+#define NQ_ABI_VERSION 2
 
 /* Packed 16-byte frontier record (one LDG.128 per refill on the device).
  *   cols      occupied columns of the first placed_rows rows   (Subproblem::cur)
@@ -156,7 +156,11 @@ int nq_partition_uniform(uint64_t task_count, int worker_count, uint64_t* ranges
 int nq_partition_weighted(uint64_t task_count, const double* weights, int worker_count,
                           uint64_t* ranges);
 
-/* --- multi-GPU execution (scheduler.hpp:266 / :573) -------------------------------- */
+/* --- multi-GPU execution (scheduler.hpp:266 / :573) --------------------------------
+ * One host thread per worker; worker w runs on devices[w % G] with its own pooled
+ * contexts (workers that share a device get distinct ones). The dynamic strategies keep
+ * two launches in flight per worker on two streams, so the next chunk's blocks fill the
+ * SMs the previous chunk's tail frees. */
 #define NQ_PARTITION_UNIFORM 0  /* PartitionStrategy::uniform  (scheduler.hpp:26)        */
 #define NQ_PARTITION_WEIGHTED 1 /* PartitionStrategy::weighted                          */
 #define NQ_PARTITION_STEALING 2 /* PartitionStrategy::stealing: fixed chunks, cursor    */
@@ -175,6 +179,29 @@ int nq_format_log(int kind, int i, uint64_t u, double d, char* buf, uint64_t cap
 
 typedef void (*nq_log_fn)(void* user, const char* line);
 
+/* --- host-side dynamic chunk dispenser (scheduler.hpp:351-362) --------------------- *
+ * The cursor the dynamic strategies draw chunks from. In one process the scheduler makes
+ * its own; a NAMED dispenser lives in a POSIX shared-memory segment, so that cooperating
+ * processes on one node (e.g. one per GPU under torchrun) share ONE dynamic dispatch —
+ * host-side, lock-free, no device collective. strategy: NQ_PARTITION_STEALING (fixed
+ * chunks, stream order) or NQ_PARTITION_GUIDED (max(remaining / 2W, floor) records from
+ * the expensive end; chunk = floor, 0 = count / (128 W)). Each process posts its partial
+ * into its own slot; nq_dispatch_sum adds the slots (checked). */
+typedef struct nq_dispatch nq_dispatch;
+int nq_dispatch_create(const char* shm_name /* NULL = in-process */, uint64_t count, int strategy,
+                       uint64_t chunk, int workers, nq_dispatch** out);
+int nq_dispatch_attach(const char* shm_name, nq_dispatch** out);
+void nq_dispatch_close(nq_dispatch* d, int unlink_segment);
+/* 1 = [*first, *first + *len) is this caller's, 0 = drained, < 0 = error. */
+int nq_dispatch_take(nq_dispatch* d, uint64_t* first, uint64_t* len);
+int nq_dispatch_reset(nq_dispatch* d); /* start a new pass over the same records */
+int nq_dispatch_info(const nq_dispatch* d, uint64_t* count, int* strategy, uint64_t* chunk,
+                     int* workers);
+int nq_dispatch_post(nq_dispatch* d, int slot, uint64_t solutions, uint64_t nodes,
+                     uint64_t processed);
+int nq_dispatch_sum(nq_dispatch* d, int slots, uint64_t* solutions, uint64_t* nodes,
+                    uint64_t* processed);
+
 typedef struct nq_solve_opts {
   int variant;                 /* NQ_VARIANT_*                                          */
   int strategy;                /* NQ_PARTITION_*                                        */
@@ -189,6 +216,9 @@ typedef struct nq_solve_opts {
   const char* config_name;     /* for the require_feasible message                        */
   nq_log_fn log;               /* optional start/finish line sink (called concurrently) */
   void* log_user;
+  nq_dispatch* dispatch;       /* stealing / guided: draw chunks from this (possibly shared) */
+                               /* dispenser instead of a private one; its count, strategy */
+                               /* and chunk win                                            */
 } nq_solve_opts;
 
 #define NQ_MAX_WORKERS 64
@@ -202,7 +232,9 @@ typedef struct nq_worker_stats {
   uint64_t nodes;              /* Alg. 3 nodes                                          */
   uint64_t chunks;             /* kernel launches                                       */
   double elapsed_ms;           /* host wall time of this worker thread                  */
-  double kernel_ms;            /* Σ device time of its launches                         */
+  double kernel_ms;            /* Σ device time of its launches (they may overlap)      */
+  double span_ms;              /* device time from its first enqueued operation to the  */
+                               /* end of its last kernel (CUDA events, one device)       */
 } nq_worker_stats;
 
 typedef struct nq_report {
@@ -219,6 +251,12 @@ typedef struct nq_report {
 int nq_solve_batch(int n, int pre_rows, const nq_sub* host_subs, uint64_t count,
                    const nq_solve_opts* opts, nq_report* out);
 int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out);
+/* execute_batch over a frontier already RESIDENT on every device: dev_subs[i] is a full
+ * copy of the count records on the i-th device of the worker device list (opts->devices,
+ * or 0..n_devices-1). Workers launch on sub-ranges of their device's copy, so only the
+ * 64-byte results cross PCIe. Strategies: uniform, weighted, stealing, guided. */
+int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* dev_subs, uint64_t count,
+                          const nq_solve_opts* opts, nq_report* out);
 
 /* --- checkpoint / resume (runner.hpp:48-212, checkpoint.hpp:21-199) -- */
 typedef struct nq_ckpt_opts {

@@ -116,6 +116,7 @@ struct WorkerStats {
     std::uint64_t nodes = 0;        ///< Alg. 3 DFS nodes counted by this worker
     std::uint64_t launches = 0;     ///< kernel launches (chunks)
     double kernel_ms = 0;           ///< device time of those launches (CUDA events)
+    double span_ms = 0;             ///< device time, first enqueued operation -> last kernel end
 };
 
 struct SolveReport {
@@ -357,6 +358,7 @@ inline SolveReport to_report(int n, int pre_rows, const ExecuteOptions& opts,
         d.nodes = s.nodes;
         d.launches = s.chunks;
         d.kernel_ms = s.kernel_ms;
+        d.span_ms = s.span_ms;
         if (opts.progress && s.assigned)
             opts.progress->commit(w, WorkerProgress{s.processed, s.partial_sum});
     }
@@ -426,6 +428,7 @@ inline SolveReport execute_checkpointed(int n, int pre_rows, const ExecuteOption
         d.nodes = rep.workers[w].nodes;
         d.launches = rep.workers[w].chunks;
         d.kernel_ms = rep.workers[w].kernel_ms;
+        d.span_ms = rep.workers[w].span_ms;
         report.workers.push_back(d);
     }
     return report;

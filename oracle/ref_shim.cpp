@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "nqueens/bankmodel.hpp"
 #include "nqueens/scheduler.hpp"
 #include "nqueens/solver.hpp"
 #include "nqueens/subproblems.hpp"
@@ -82,6 +83,40 @@ int nqref_generate(int n, int pre_rows, Packed* out, uint64_t cap, uint64_t* tot
       ++len;
     });
     *total = len;
+  });
+}
+
+// Records i ≡ offset (mod stride) of the reference stream (for_each_subproblem,
+// subproblems.hpp:80-108), so bench.py's reference arm builds its sample with the
+// reference's own generator and never loads the product library.
+int nqref_generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, Packed* out,
+                         uint64_t cap, uint64_t* total) {
+  return guard([&] {
+    if (stride == 0) throw nqueens::config_error("stride must be >= 1");
+    uint64_t idx = 0, len = 0;
+    nqueens::for_each_subproblem(nqueens::GenerationPlan{n, pre_rows}, [&](const nqueens::Subproblem& s) {
+      if (idx++ % stride != offset) return;
+      if (out && len < cap)
+        out[len] = Packed{s.cur, s.left, s.right,
+                          static_cast<uint32_t>(s.placed_rows) | (static_cast<uint32_t>(s.multiplier) << 8)};
+      ++len;
+    });
+    *total = len;
+  });
+}
+
+// bankmodel.hpp:62-99 (conflict_degree), so the layout self-check's restatement is
+// pinned to the reference's own model. schedule: 0 quarter_warp, 1 full_warp.
+int nqref_conflict_degree(int bank_count, int word_bytes, int warp_size, const uint64_t* addrs,
+                          uint64_t len, int width_bytes, int schedule, int* transactions,
+                          int* max_degree) {
+  return guard([&] {
+    const nqueens::BankGeometry g{bank_count, word_bytes, warp_size};
+    nqueens::AccessRequest req{std::vector<std::uint64_t>(addrs, addrs + len), width_bytes};
+    const auto r = nqueens::conflict_degree(
+        g, req, schedule ? nqueens::WarpSchedule::full_warp : nqueens::WarpSchedule::quarter_warp);
+    *transactions = r.transactions;
+    *max_degree = r.max_degree;
   });
 }
 

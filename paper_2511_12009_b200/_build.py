@@ -16,7 +16,8 @@ REPO = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO, "include")
 LIB_PATH = os.path.join(PKG_DIR, "libnqb200.so")
-SOURCES = ["nq_capi.cu", "nq_expand.cu", "nq_frontier.cpp", "nq_sched.cpp", "nq_ckpt.cpp"]
+SOURCES = ["nq_capi.cu", "nq_expand.cu", "nq_frontier.cpp", "nq_sched.cpp", "nq_ckpt.cpp",
+           "nq_dispatch.cpp"]
 HEADERS = ["nq_kernel.cuh", "nq_internal.h"]
 
 NVCC_FLAGS = [

@@ -50,7 +50,8 @@ class NqSolveOpts(ctypes.Structure):
                 ("chunk", ctypes.c_uint64), ("n_devices", ctypes.c_int),
                 ("devices", ctypes.POINTER(ctypes.c_int)), ("cancel", ctypes.POINTER(ctypes.c_int)),
                 ("stack_depth", ctypes.c_int), ("config_name", ctypes.c_char_p),
-                ("log", NQ_LOG_FN), ("log_user", ctypes.c_void_p)]
+                ("log", NQ_LOG_FN), ("log_user", ctypes.c_void_p),
+                ("dispatch", ctypes.c_void_p)]
 
 
 MAX_WORKERS = 64
@@ -61,7 +62,7 @@ class NqWorkerStats(ctypes.Structure):
                 ("assigned", ctypes.c_uint64), ("processed", ctypes.c_uint64),
                 ("partial_sum", ctypes.c_uint64), ("nodes", ctypes.c_uint64),
                 ("chunks", ctypes.c_uint64), ("elapsed_ms", ctypes.c_double),
-                ("kernel_ms", ctypes.c_double)]
+                ("kernel_ms", ctypes.c_double), ("span_ms", ctypes.c_double)]
 
 
 class NqReport(ctypes.Structure):
@@ -134,6 +135,18 @@ _sigs = {
     "nq_solve_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64,
                                       _P(NqSolveOpts), _P(NqReport)]),
     "nq_solve": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts), _P(NqReport)]),
+    "nq_solve_batch_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(ctypes.c_void_p), _u64,
+                                             _P(NqSolveOpts), _P(NqReport)]),
+    "nq_dispatch_create": (ctypes.c_int, [ctypes.c_char_p, _u64, ctypes.c_int, _u64, ctypes.c_int,
+                                          _P(ctypes.c_void_p)]),
+    "nq_dispatch_attach": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_void_p)]),
+    "nq_dispatch_close": (None, [ctypes.c_void_p, ctypes.c_int]),
+    "nq_dispatch_take": (ctypes.c_int, [ctypes.c_void_p, _P(_u64), _P(_u64)]),
+    "nq_dispatch_reset": (ctypes.c_int, [ctypes.c_void_p]),
+    "nq_dispatch_info": (ctypes.c_int, [ctypes.c_void_p, _P(_u64), _P(ctypes.c_int), _P(_u64),
+                                        _P(ctypes.c_int)]),
+    "nq_dispatch_post": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u64, _u64, _u64]),
+    "nq_dispatch_sum": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _P(_u64), _P(_u64), _P(_u64)]),
     "nq_solve_checkpointed": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts),
                                              _P(NqCkptOpts), _P(NqReport)]),
     "nq_checkpoint_read": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_int), _P(ctypes.c_int),

@@ -103,6 +103,7 @@ struct nq_ctx {
   cudaStream_t side = nullptr;             // carries the cancel word while a launch runs
   const volatile int* cancel = nullptr;    // host flag polled while waiting (may be null)
   cudaEvent_t ev_h2d = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
+  cudaEvent_t ev_start = nullptr;          // a worker's first enqueued operation (span)
   uint4* d_subs = nullptr;
   size_t d_cap = 0;                        // records
   unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals, [6] stop word
@@ -116,6 +117,7 @@ struct nq_ctx {
   bool pending = false;
   int p_variant = 1;
   bool p_h2d = false;
+  int p_pre_rows = 0;
   uint64_t p_count = 0;
   uint64_t last_bad = ~0ull;               // index (within the batch) of a rejected record
   uint64_t last_expanded = 0;              // records produced by the last nq_count_expand
@@ -132,6 +134,29 @@ uint64_t ctx_last_expanded(const nq_ctx* c) { return c->last_expanded; }
 
 namespace {
 
+// Every kernel instantiation may take the device's whole opt-in shared memory, set ONCE
+// per device (at context creation): setting it per launch to that launch's size let a
+// concurrent smaller launch on another context lower the limit between a larger
+// launch's set and its launch. Occupancy is still computed from the real size.
+int set_kernel_attributes(int device) {
+  static std::mutex mu;
+  static std::vector<bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(done.size()) <= device) done.resize(device + 1, false);
+  if (done[device]) return NQ_OK;
+  int optin = 0;
+  NQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  for (int block : {64, 96, 128, 192, 256})
+    for (bool per_sub : {false, true})
+      for (int layout : {NQ_LAYOUT_V4, NQ_LAYOUT_PLANES}) {
+        KernelFn fn = kernel_for(block, per_sub, layout);
+        NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
+  done[device] = true;
+  return NQ_OK;
+}
+
 struct Launch {
   int grid = 0;
   size_t smem = 0;
@@ -144,9 +169,6 @@ int plan_launch(nq_ctx* c, int n, int pre_rows, bool per_sub, Launch* L) {
   L->fn = kernel_for(c->block, per_sub, c->layout);
   if (!L->fn) return set_error(NQ_ECONFIG, "unsupported block size " + std::to_string(c->block));
   L->smem = static_cast<size_t>(levels) * c->block * 16u;
-  NQ_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(L->smem)));
-  NQ_CUDA(cudaFuncSetAttribute(L->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   NQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, c->block, L->smem));
   if (per_sm < 1)
@@ -270,6 +292,81 @@ int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
 
 }  // namespace
 
+namespace nqb200 {
+
+int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, uint64_t count,
+               int kind) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (c->pending) return set_error(NQ_ECONFIG, "a batch is already in flight on this context");
+  if (int rc = check_args(n, pre_rows, variant)) return rc;
+  NQ_CUDA(cudaSetDevice(c->device));
+  c->last_bad = ~0ull;
+  const nq_sub* dev = subs;
+  if (kind == kLaunchHost) {
+    if (int rc = ensure_capacity(c, count)) return rc;
+    NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
+    if (count)
+      NQ_CUDA(cudaMemcpyAsync(c->d_subs, subs, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                              c->stream));
+    dev = reinterpret_cast<const nq_sub*>(c->d_subs);
+  } else if (kind == kLaunchExpand) {
+    // Only the coarse roots cross PCIe; the level buffers come from the device's
+    // stream-ordered pool and are released on the same stream behind the kernel.
+    NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
+    uint4* d_roots = nullptr;
+    NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), std::max<uint64_t>(count, 1) * 16,
+                            c->stream));
+    struct Free {
+      uint4* p;
+      cudaStream_t s;
+      ~Free() {
+        if (p) cudaFreeAsync(p, s);
+      }
+    } roots_guard{d_roots, c->stream}, deep_guard{nullptr, c->stream};
+    if (count)
+      NQ_CUDA(cudaMemcpyAsync(d_roots, subs, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                              c->stream));
+    uint64_t total = 0;
+    if (int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
+                               pre_rows, c->stream, &deep_guard.p, &total))
+      return rc;
+    c->last_expanded = total;
+    if (int rc = enqueue(c, n, pre_rows, variant, reinterpret_cast<const nq_sub*>(deep_guard.p),
+                         total, false, nullptr, nullptr, nullptr))
+      return rc;
+    c->pending = true;
+    c->p_variant = variant;
+    c->p_h2d = true;
+    c->p_pre_rows = pre_rows;
+    c->p_count = total;
+    return NQ_OK;
+  }
+  if (int rc = enqueue(c, n, pre_rows, variant, dev, count, false, nullptr, nullptr, nullptr))
+    return rc;
+  c->pending = true;
+  c->p_variant = variant;
+  c->p_h2d = kind == kLaunchHost;
+  c->p_pre_rows = pre_rows;
+  c->p_count = count;
+  return NQ_OK;
+}
+
+int ctx_mark_start(nq_ctx* c) {
+  NQ_CUDA(cudaSetDevice(c->device));
+  NQ_CUDA(cudaEventRecord(c->ev_start, c->stream));
+  return NQ_OK;
+}
+
+double ctx_span_ms(const nq_ctx* start, const nq_ctx* end) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, start->ev_start, end->ev_k1) != cudaSuccess) return 0.0;
+  return ms;
+}
+
+int ctx_device(const nq_ctx* c) { return c->device; }
+
+}  // namespace nqb200
+
 // ---- C ABI ------------------------------------------------------------------------------
 extern "C" {
 
@@ -305,6 +402,8 @@ int nq_ctx_create(int device, nq_ctx** out) {
   NQ_CUDA(cudaEventCreate(&c->ev_h2d));
   NQ_CUDA(cudaEventCreate(&c->ev_k0));
   NQ_CUDA(cudaEventCreate(&c->ev_k1));
+  NQ_CUDA(cudaEventCreate(&c->ev_start));
+  if (int rc = set_kernel_attributes(device)) return rc;
   NQ_CUDA(cudaMalloc(&c->d_ctl, 8 * sizeof(unsigned long long)));
   NQ_CUDA(cudaMallocHost(&c->h_ctl, 16 * sizeof(unsigned long long)));
   *out = c.release();
@@ -321,6 +420,7 @@ void nq_ctx_destroy(nq_ctx* c) {
   if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
   if (c->ev_k0) cudaEventDestroy(c->ev_k0);
   if (c->ev_k1) cudaEventDestroy(c->ev_k1);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;
@@ -361,87 +461,39 @@ int nq_ctx_set_layout(nq_ctx* c, int layout) {
 
 int nq_count_device_async(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
                           uint64_t count) {
-  if (!c) return set_error(NQ_ECONFIG, "null context");
-  if (c->pending) return set_error(NQ_ECONFIG, "a batch is already in flight on this context");
-  if (int rc = check_args(n, pre_rows, variant)) return rc;
-  NQ_CUDA(cudaSetDevice(c->device));
-  if (int rc = enqueue(c, n, pre_rows, variant, dev_subs, count, false, nullptr, nullptr, nullptr))
-    return rc;
-  c->pending = true;
-  c->p_variant = variant;
-  c->p_h2d = false;
-  c->p_count = count;
-  return NQ_OK;
+  return nqb200::ctx_launch(c, n, pre_rows, variant, dev_subs, count, nqb200::kLaunchDevice);
 }
 
 int nq_collect(nq_ctx* c, nq_result* out) {
   if (!c || !c->pending) return set_error(NQ_ECONFIG, "no batch in flight");
   c->pending = false;
   NQ_CUDA(cudaSetDevice(c->device));
-  return finish(c, c->p_variant, c->p_h2d, 0, out);
+  return finish(c, c->p_variant, c->p_h2d, c->p_pre_rows, out);
 }
 
 int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
                     uint64_t count, nq_result* out) {
-  if (!c) return set_error(NQ_ECONFIG, "null context");
-  if (int rc = check_idle(c)) return rc;
   NvtxRange range("nq_count_device (DFS kernel + D2H)");
-  if (int rc = check_args(n, pre_rows, variant)) return rc;
-  NQ_CUDA(cudaSetDevice(c->device));
-  if (int rc = enqueue(c, n, pre_rows, variant, dev_subs, count, false, nullptr, nullptr, nullptr))
+  if (int rc = nqb200::ctx_launch(c, n, pre_rows, variant, dev_subs, count, nqb200::kLaunchDevice))
     return rc;
-  return finish(c, variant, false, pre_rows, out);
+  return nq_collect(c, out);
 }
 
 int nq_count(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs, uint64_t count,
              nq_result* out) {
-  if (!c) return set_error(NQ_ECONFIG, "null context");
-  if (int rc = check_idle(c)) return rc;
   NvtxRange range("nq_count (H2D + DFS kernel + D2H)");
-  if (int rc = check_args(n, pre_rows, variant)) return rc;
-  NQ_CUDA(cudaSetDevice(c->device));
-  if (int rc = ensure_capacity(c, count)) return rc;
-  NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
-  if (count)
-    NQ_CUDA(cudaMemcpyAsync(c->d_subs, host_subs, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
-                            c->stream));
-  if (int rc = enqueue(c, n, pre_rows, variant, reinterpret_cast<const nq_sub*>(c->d_subs), count,
-                       false, nullptr, nullptr, nullptr))
+  if (int rc = nqb200::ctx_launch(c, n, pre_rows, variant, host_subs, count, nqb200::kLaunchHost))
     return rc;
-  return finish(c, variant, true, pre_rows, out);
+  return nq_collect(c, out);
 }
 
 int nq_count_expand(nq_ctx* c, int n, int target_rows, int variant, const nq_sub* host_roots,
                     uint64_t count, nq_result* out) {
-  if (!c) return set_error(NQ_ECONFIG, "null context");
-  if (int rc = check_idle(c)) return rc;
-  if (int rc = check_args(n, target_rows, variant)) return rc;
   NvtxRange range("nq_count_expand (H2D roots + device deepening + DFS kernel)");
-  NQ_CUDA(cudaSetDevice(c->device));
-  NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
-  uint4* d_roots = nullptr;
-  NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), std::max<uint64_t>(count, 1) * 16,
-                          c->stream));
-  struct Free {
-    uint4* p;
-    cudaStream_t s;
-    ~Free() {
-      if (p) cudaFreeAsync(p, s);
-    }
-  } roots_guard{d_roots, c->stream}, deep_guard{nullptr, c->stream};
-  if (count)
-    NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
-                            c->stream));
-  uint64_t total = 0;
-  // Deepen on the context's own stream (ordered after the copy), then count in place.
-  if (int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
-                             target_rows, c->stream, &deep_guard.p, &total))
+  if (int rc = nqb200::ctx_launch(c, n, target_rows, variant, host_roots, count,
+                                  nqb200::kLaunchExpand))
     return rc;
-  c->last_expanded = total;
-  if (int rc = enqueue(c, n, target_rows, variant, reinterpret_cast<const nq_sub*>(deep_guard.p),
-                       total, false, nullptr, nullptr, nullptr))
-    return rc;
-  return finish(c, variant, true, target_rows, out);
+  return nq_collect(c, out);
 }
 
 int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* host_subs,

@@ -45,10 +45,24 @@ uint64_t ctx_last_bad(const nq_ctx* c);
 // Records the last nq_count_expand deepened (the launch's full work, for cancel checks).
 uint64_t ctx_last_expanded(const nq_ctx* c);
 
+// Asynchronous launch on a context (completed by nq_collect): host records (H2D into the
+// context's buffer), device-resident records, or host roots deepened to pre_rows on the
+// device first. The scheduler's workers keep two of these in flight on two contexts.
+enum { kLaunchHost = 0, kLaunchDevice = 1, kLaunchExpand = 2 };
+int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, uint64_t count,
+               int kind);
+// Marks a worker's start on c's stream; ctx_span_ms(start, end) is the device time from
+// that mark to the end of end's last kernel (both contexts on one device).
+int ctx_mark_start(nq_ctx* c);
+double ctx_span_ms(const nq_ctx* start, const nq_ctx* end);
+int ctx_device(const nq_ctx* c);
+
 // execute_batch over records that are deepened to `target_rows` on the device first
 // (target_rows == 0: count the records as they are). nq_solve_batch is the
 // target_rows == 0 case; nq_solve uses the deepening form for large frontiers.
-int solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs, uint64_t count,
-                     const nq_solve_opts* opts, nq_report* out);
+// dev_subs (optional): per worker-device full copies of subs already on the devices.
+int solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs,
+                     const nq_sub* const* dev_subs, uint64_t count, const nq_solve_opts* opts,
+                     nq_report* out);
 
 }  // namespace nqb200

@@ -148,11 +148,18 @@ extern "C" int nq_partition_weighted(uint64_t task_count, const double* weights,
 
 extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t count,
                               const nq_solve_opts* opts, nq_report* out) {
-  return solve_batch_impl(n, pre_rows, 0, subs, count, opts, out);
+  return solve_batch_impl(n, pre_rows, 0, subs, nullptr, count, opts, out);
+}
+
+extern "C" int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* dev_subs,
+                                     uint64_t count, const nq_solve_opts* opts, nq_report* out) {
+  if (!dev_subs) return set_error(NQ_ECONFIG, "null device frontier list");
+  return solve_batch_impl(n, pre_rows, 0, nullptr, dev_subs, count, opts, out);
 }
 
 int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs,
-                             uint64_t count, const nq_solve_opts* opts, nq_report* out) {
+                             const nq_sub* const* dev_subs, uint64_t count,
+                             const nq_solve_opts* opts, nq_report* out) {
   using clk = std::chrono::steady_clock;
   // The pooled per-device contexts are shared by every call: concurrent calls from
   // different host threads run one after the other (the reference's execute_batch is
@@ -164,6 +171,13 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
   o.variant = NQ_VARIANT_LASTROW;
   o.strategy = NQ_PARTITION_STRIDED;
   if (opts) o = *opts;
+  if (o.dispatch) {  // a shared dispenser fixes the policy for every cooperating caller
+    uint64_t d_count = 0;
+    nq_dispatch_info(o.dispatch, &d_count, &o.strategy, &o.chunk, nullptr);
+    if (d_count != count)
+      return set_error(NQ_ECONFIG, "dispenser covers " + std::to_string(d_count) +
+                                       " records but the batch has " + std::to_string(count));
+  }
   if (o.worker_count < 0) return set_error(NQ_ECONFIG, "worker_count must be >= 1");
   if (o.strategy == NQ_PARTITION_STEALING && o.chunk == 0)
     return set_error(NQ_ECONFIG, "chunk_size must be >= 1");
@@ -173,11 +187,13 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
                                 target_rows ? target_rows : pre_rows,
                                 o.variant == NQ_VARIANT_LASTROW))
     return rc;
-  if (target_rows && o.strategy != NQ_PARTITION_STRIDED)
-    return set_error(NQ_ECONFIG, "device-side deepening needs the strided strategy");
-  if (n < 1 || n > 31)
-    return set_error(NQ_ECONFIG, "board size must be in [1, 31] on the GPU path, got " +
-                                     std::to_string(n));
+  if (target_rows && o.strategy != NQ_PARTITION_STRIDED && o.strategy != NQ_PARTITION_GUIDED)
+    return set_error(NQ_ECONFIG, "device-side deepening needs the strided or guided strategy");
+  if (dev_subs && o.strategy == NQ_PARTITION_STRIDED)
+    return set_error(NQ_ECONFIG, "a device-resident frontier is split by ranges or chunks "
+                                 "(uniform, weighted, stealing, guided), not strided");
+  if (n < 1 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
 
   int ndev = 0;
   if (int rc = nq_device_count(&ndev)) return rc;
@@ -193,6 +209,12 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
   const int W = o.worker_count > 0 ? o.worker_count : G;
   if (W > NQ_MAX_WORKERS)
     return set_error(NQ_ECONFIG, "worker_count above " + std::to_string(NQ_MAX_WORKERS));
+  // Worker w runs on devs[w % G]. Its context slot is the number of earlier workers on
+  // the same device id, so two workers never share a context (stream, buffers, result
+  // mirror) even when the device list repeats a device (devices = {0, 0, ...}).
+  std::vector<int> slot(W, 0);
+  for (int w = 0; w < W; ++w)
+    for (int v = 0; v < w; ++v) slot[w] += devs[v % G] == devs[w % G] ? 1 : 0;
 
   std::vector<uint64_t> ranges;
   if (o.strategy == NQ_PARTITION_UNIFORM || o.strategy == NQ_PARTITION_WEIGHTED) {
@@ -210,35 +232,23 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
     }
     if (rc) return rc;
   }
+  const bool dynamic = o.strategy == NQ_PARTITION_STEALING || o.strategy == NQ_PARTITION_GUIDED;
+  nq_dispatch* disp = o.dispatch;
+  struct DispGuard {
+    nq_dispatch* d = nullptr;
+    ~DispGuard() { nq_dispatch_close(d, 0); }
+  } own_disp;
+  if (dynamic && !disp) {
+    if (int rc = nq_dispatch_create(nullptr, count, o.strategy, o.chunk, W, &own_disp.d)) return rc;
+    disp = own_disp.d;
+  }
 
   std::memset(out, 0, sizeof(*out));
   out->task_count = count;
   out->worker_count = W;
 
-  // Dynamic dispensers. stealing: fixed chunks in stream order (scheduler.hpp:356-361);
-  // guided: max(remaining / 2W, floor) from the back of the stream.
-  std::atomic<uint64_t> cursor{0};
-  std::mutex guided_mu;
-  uint64_t guided_taken = 0;
-  const uint64_t guided_floor = o.chunk ? o.chunk : std::max<uint64_t>(count / (16ull * W), 4096);
-  auto take = [&](uint64_t* first, uint64_t* len) -> bool {
-    if (o.strategy == NQ_PARTITION_STEALING) {
-      const uint64_t f = cursor.fetch_add(o.chunk, std::memory_order_relaxed);
-      if (f >= count) return false;
-      *first = f;
-      *len = std::min(o.chunk, count - f);
-      return true;
-    }
-    std::lock_guard<std::mutex> lk(guided_mu);
-    if (guided_taken >= count) return false;
-    const uint64_t rem = count - guided_taken;
-    const uint64_t sz = std::min(rem, std::max<uint64_t>(rem / (2ull * W), guided_floor));
-    *first = count - guided_taken - sz;
-    *len = sz;
-    guided_taken += sz;
-    return true;
-  };
-
+  const int kind = target_rows ? kLaunchExpand : (dev_subs ? kLaunchDevice : kLaunchHost);
+  const int launch_rows = target_rows ? target_rows : pre_rows;
   std::atomic<bool> interrupted{false};
   std::mutex fail_mu;
   std::string failure;
@@ -250,31 +260,61 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
       nq_worker_stats& st = out->workers[w];
       st.worker = w;
       st.device = devs[w % G];
+      const nq_sub* src = dev_subs ? dev_subs[w % G] : subs;
       const std::string range_name = "nq_solve_batch worker " + std::to_string(w);
       NvtxRange range(range_name.c_str());
       const auto s0 = clk::now();
-      uint64_t first = 0, len = 0;
-      nq_ctx* c = nullptr;
-      int rc = pooled_ctx(st.device, w / G, &c);
-      if (rc == NQ_OK) nq_ctx_set_cancel(c, o.cancel);
-      auto run = [&](uint64_t f, uint64_t l) -> int {
+      // Two contexts per worker: dynamic strategies keep one launch running while the
+      // next is enqueued, so a chunk's tail overlaps the next chunk's first blocks.
+      nq_ctx* cx[2] = {nullptr, nullptr};
+      struct Flight {
+        bool busy = false;
+        uint64_t first = 0, len = 0, work = 0;
+      } fl[2];
+      uint64_t bad_first = 0, bad_len = 0;  // the launch that failed (for the message)
+      bool strided_index = false;
+      int rc = pooled_ctx(st.device, 2 * slot[w], &cx[0]);
+      if (rc == NQ_OK && dynamic) rc = pooled_ctx(st.device, 2 * slot[w] + 1, &cx[1]);
+      for (nq_ctx* c : cx)
+        if (c) nq_ctx_set_cancel(c, o.cancel);
+      if (rc == NQ_OK) rc = ctx_mark_start(cx[0]);
+      auto launch = [&](int i, const nq_sub* base, uint64_t f, uint64_t l) -> int {
+        const int e = ctx_launch(cx[i], n, launch_rows, o.variant, base + f, l, kind);
+        if (e) {
+          bad_first = f;
+          bad_len = l;
+          return e;
+        }
+        fl[i].busy = true;
+        fl[i].first = f;
+        fl[i].len = l;
+        fl[i].work = kind == kLaunchExpand ? ctx_last_expanded(cx[i]) : l;
+        return NQ_OK;
+      };
+      auto collect = [&](int i) -> int {
         nq_result r{};
-        int e = nq_count(c, n, pre_rows, o.variant, subs + f, l, &r);
-        if (e) return e;
-        if (r.subproblems < l) interrupted.store(true);  // cancelled inside the launch
+        fl[i].busy = false;
+        const int e = nq_collect(cx[i], &r);
+        if (e) {
+          bad_first = fl[i].first;
+          bad_len = fl[i].len;
+          return e;
+        }
+        if (r.subproblems < fl[i].work) interrupted.store(true);  // cancelled inside the launch
         if (!add_ok(st.partial_sum, r.solutions, &st.partial_sum))
           return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
         st.processed += r.subproblems;
         st.nodes += r.nodes;
         st.chunks += 1;
         st.kernel_ms += r.kernel_ms;
+        st.span_ms = std::max(st.span_ms, ctx_span_ms(cx[0], cx[i]));
         return NQ_OK;
       };
+      std::vector<nq_sub> gathered;
       if (rc == NQ_OK) {
         if (o.strategy == NQ_PARTITION_STRIDED) {
           // Gather records w, w+W, w+2W, ... and count them in one launch (a single
           // worker counts the caller's buffer in place: no host copy).
-          std::vector<nq_sub> gathered;
           const nq_sub* mine = subs;
           uint64_t mine_n = count;
           if (W > 1) {
@@ -284,62 +324,70 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
             mine = gathered.data();
             mine_n = gathered.size();
           }
+          strided_index = true;
           st.assigned = mine_n;
           emit(o, NQ_LOG_START, w, mine_n, count ? double(mine_n) / double(count) : 0.0);
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (mine_n) {
-            nq_result r{};
-            uint64_t work = mine_n;
-            if (target_rows) {  // coarse roots: deepened and counted on the device
-              rc = nq_count_expand(c, n, target_rows, o.variant, mine, mine_n, &r);
-              work = ctx_last_expanded(c);
-            } else {
-              rc = nq_count(c, n, pre_rows, o.variant, mine, mine_n, &r);
-            }
-            if (rc == NQ_OK) {
-              if (r.subproblems < work) interrupted.store(true);
-              st.partial_sum = r.solutions;
-              st.processed = r.subproblems;
-              st.nodes = r.nodes;
-              st.chunks = 1;
-              st.kernel_ms = r.kernel_ms;
-            }
+            rc = launch(0, mine, 0, mine_n);
+            if (rc == NQ_OK) rc = collect(0);
           }
         } else if (!ranges.empty()) {
-          first = ranges[2 * w];
-          len = ranges[2 * w + 1] - first;
+          const uint64_t first = ranges[2 * w], len = ranges[2 * w + 1] - first;
           st.assigned = len;
           emit(o, NQ_LOG_START, w, len, count ? double(len) / double(count) : 0.0);
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (len) {
-            rc = run(first, len);
+            rc = launch(0, src, first, len);
+            if (rc == NQ_OK) rc = collect(0);
           }
         } else {
           emit(o, NQ_LOG_START, w, 0, 0.0);
+          int cur = 0;
           while (rc == NQ_OK && !interrupted.load()) {
             if (cancel_raised(o.cancel)) {
               interrupted.store(true);
               break;
             }
-            if (!take(&first, &len)) break;
-            rc = run(first, len);
+            uint64_t f = 0, l = 0;
+            const int got = nq_dispatch_take(disp, &f, &l);
+            if (got < 0) {
+              rc = got;
+              break;
+            }
+            if (got == 0) break;
+            if (fl[cur].busy) rc = collect(cur);  // the launch issued two chunks ago
+            if (rc == NQ_OK) rc = launch(cur, src, f, l);
+            cur ^= 1;
+          }
+          // Drain: the older launch first.
+          for (int k = 0; k < 2; ++k) {
+            const int i = cur ^ k;
+            if (fl[i].busy) {
+              const int e = collect(i);
+              if (rc == NQ_OK) rc = e;
+            }
           }
         }
       }
       st.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - s0).count();
-      if (c) nq_ctx_set_cancel(c, nullptr);
+      for (nq_ctx* c : cx)
+        if (c) nq_ctx_set_cancel(c, nullptr);
       if (rc) {
         std::lock_guard<std::mutex> lk(fail_mu);
         if (failure.empty()) {
-          const uint64_t bad = c ? ctx_last_bad(c) : ~0ull;
-          const uint64_t global_bad = o.strategy == NQ_PARTITION_STRIDED
+          uint64_t bad = ~0ull;
+          for (nq_ctx* c : cx)
+            if (c && ctx_last_bad(c) != ~0ull) bad = ctx_last_bad(c);
+          const uint64_t global_bad = strided_index
                                           ? static_cast<uint64_t>(w) + bad * static_cast<uint64_t>(W)
-                                          : first + bad;
-          std::string where = bad != ~0ull ? "subproblem " + std::to_string(global_bad)
-                                           : "chunk [" + std::to_string(first) + ", " +
-                                                 std::to_string(first + len) + ")";
+                                          : bad_first + bad;
+          std::string where = bad != ~0ull && kind != kLaunchExpand
+                                  ? "subproblem " + std::to_string(global_bad)
+                                  : "chunk [" + std::to_string(bad_first) + ", " +
+                                        std::to_string(bad_first + bad_len) + ")";
           failure = "worker " + std::to_string(w) + " failed on " + where + ": " + nq_last_error();
         }
         interrupted.store(true);
@@ -386,21 +434,23 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   uint64_t total = 0;
   if (int rc = count_subproblems(n, pre_rows, &total)) return rc;
   // Large frontiers (N=27, R=7: 453,688,251 records, 7.26 GB) are never materialised on
-  // the host: a coarse frontier 3 rows shallower is dealt to the workers and deepened on
-  // each device (nq_count_expand). From ~1 M records up this is also the faster path —
+  // the host: a coarse frontier 3 rows shallower is dealt to the workers (strided shares,
+  // or guided chunks of roots) and deepened on each device (nq_count_expand). From ~1 M records up this is also the faster path —
   // N=20 R=7 execute: 1 573 ms vs 1 716 ms with host generation + 364 MB H2D — so it is
   // the default there. Threshold: NQB_DEVICE_EXPAND_MIN_RECORDS (default 2^20).
   uint64_t expand_min = 1ull << 20;
   if (const char* e = std::getenv("NQB_DEVICE_EXPAND_MIN_RECORDS")) expand_min = std::strtoull(e, nullptr, 10);
   const int coarse = std::max(2, pre_rows - 3);
-  if (total >= expand_min && o.strategy == NQ_PARTITION_STRIDED && coarse < pre_rows) {
+  const bool deepenable = o.strategy == NQ_PARTITION_STRIDED ||
+                          (o.strategy == NQ_PARTITION_GUIDED && !o.dispatch);
+  if (total >= expand_min && deepenable && coarse < pre_rows) {
     uint64_t roots_n = 0;
     if (int rc = count_subproblems(n, coarse, &roots_n)) return rc;
     std::vector<nq_sub> roots(roots_n);
     if (int rc = generate_slice(n, coarse, 1, 0, roots.data(), roots_n, &roots_n)) return rc;
     const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
     emit(o, NQ_LOG_GENERATION, 0, total, gen_ms);
-    const int rc = solve_batch_impl(n, coarse, pre_rows, roots.data(), roots_n, &o, out);
+    const int rc = solve_batch_impl(n, coarse, pre_rows, roots.data(), nullptr, roots_n, &o, out);
     if (rc) return rc;
     out->task_count = total;
     out->generation_ms = gen_ms;

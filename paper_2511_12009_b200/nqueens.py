@@ -404,6 +404,7 @@ class WorkerStats:
     nodes: int = 0
     kernel_ms: float = 0.0
     chunks: int = 0
+    span_ms: float = 0.0  # device time, first enqueued operation -> last kernel end
 
 
 @dataclass
@@ -474,6 +475,7 @@ class ExecuteOptions:
     cancel: Optional[threading.Event] = None
     resume: list = field(default_factory=list)
     devices: Optional[Sequence[int]] = None  # GPU extension: explicit device list
+    dispatch: Optional["Dispatcher"] = None  # GPU extension: shared dynamic dispenser
 
 
 class _CancelWatch:
@@ -521,6 +523,8 @@ def _solve_opts(opts: ExecuteOptions, keep: list):
         keep.append(d)
         o.devices = d
         o.n_devices = len(opts.devices)
+    if opts.dispatch is not None:
+        o.dispatch = opts.dispatch.handle
     o.stack_depth = opts.config.max_depth()
     name = opts.config.name.encode()
     keep.append(name)
@@ -550,7 +554,7 @@ def _report(n: int, pre_rows: int, opts: ExecuteOptions, rep) -> SolveReport:
         r.workers.append(WorkerStats(worker=w.worker, assigned=w.assigned, processed=w.processed,
                                      partial_sum=w.partial_sum, elapsed_ms=w.elapsed_ms,
                                      device=w.device, nodes=w.nodes, kernel_ms=w.kernel_ms,
-                                     chunks=w.chunks))
+                                     chunks=w.chunks, span_ms=w.span_ms))
     return r
 
 
@@ -572,6 +576,89 @@ def execute_batch(n: int, pre_rows: int, batch, opts: ExecuteOptions) -> SolveRe
     finally:
         _stop_watchers(keep)
     return _report(n, pre_rows, opts, rep)
+
+
+def execute_batch_device(n: int, pre_rows: int, dev_ptrs: Sequence[int], count: int,
+                         opts: ExecuteOptions) -> SolveReport:
+    """execute_batch over a frontier already resident on every worker device
+    (nq_solve_batch_device): dev_ptrs[i] holds all `count` packed records on the i-th
+    device of opts.devices; workers launch on sub-ranges, only results cross PCIe."""
+    if opts.plan.worker_count < 1:
+        raise ConfigError("worker_count must be >= 1")
+    require_feasible(opts.config, n, pre_rows, opts.kernel is KernelVariant.lastrow)
+    keep: list = []
+    o = _solve_opts(opts, keep)
+    ptrs = (ctypes.c_void_p * len(dev_ptrs))(*dev_ptrs)
+    rep = _lib.NqReport()
+    try:
+        _call(lib.nq_solve_batch_device(n, pre_rows, ptrs, count, ctypes.byref(o), ctypes.byref(rep)))
+    finally:
+        _stop_watchers(keep)
+    return _report(n, pre_rows, opts, rep)
+
+
+class Dispatcher:
+    """The scheduler's host-side dynamic chunk dispenser (nq_dispatch_*). name=None: private
+    to this process; a name: a POSIX shared-memory segment that cooperating processes
+    (one per GPU) attach to, so they share ONE guided/stealing cursor with no device
+    collective (scheduler.hpp:351-362). Partials are posted per slot and summed checked."""
+
+    def __init__(self, handle: int, name: Optional[str], owner: bool):
+        self.handle = handle
+        self.name = name
+        self._owner = owner
+
+    @classmethod
+    def create(cls, count: int, strategy: PartitionStrategy = PartitionStrategy.guided,
+               chunk: int = 0, workers: int = 1, name: Optional[str] = None) -> "Dispatcher":
+        h = ctypes.c_void_p()
+        _call(lib.nq_dispatch_create(name.encode() if name else None, count, strategy.value,
+                                     chunk, workers, ctypes.byref(h)))
+        return cls(h.value, name, True)
+
+    @classmethod
+    def attach(cls, name: str) -> "Dispatcher":
+        h = ctypes.c_void_p()
+        _call(lib.nq_dispatch_attach(name.encode(), ctypes.byref(h)))
+        return cls(h.value, name, False)
+
+    def take(self):
+        """(first, length) of the next chunk, or None when drained."""
+        f, n = ctypes.c_uint64(), ctypes.c_uint64()
+        rc = lib.nq_dispatch_take(self.handle, ctypes.byref(f), ctypes.byref(n))
+        if rc < 0:
+            _call(rc)
+        return (f.value, n.value) if rc == 1 else None
+
+    def reset(self) -> None:
+        _call(lib.nq_dispatch_reset(self.handle))
+
+    def info(self) -> dict:
+        c, s, k, w = ctypes.c_uint64(), ctypes.c_int(), ctypes.c_uint64(), ctypes.c_int()
+        _call(lib.nq_dispatch_info(self.handle, ctypes.byref(c), ctypes.byref(s), ctypes.byref(k),
+                                   ctypes.byref(w)))
+        return {"count": c.value, "strategy": PartitionStrategy(s.value), "chunk": k.value,
+                "workers": w.value}
+
+    def post(self, slot: int, solutions: int, nodes: int, processed: int) -> None:
+        _call(lib.nq_dispatch_post(self.handle, slot, solutions, nodes, processed))
+
+    def sum(self, slots: int):
+        """(solutions, nodes, processed) over slots 0..slots-1 (every slot must have posted)."""
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _call(lib.nq_dispatch_sum(self.handle, slots, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def close(self, unlink: Optional[bool] = None) -> None:
+        if self.handle:
+            lib.nq_dispatch_close(self.handle, int(self._owner if unlink is None else unlink))
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
 
 def execute(n: int, pre_rows: int, opts: ExecuteOptions) -> SolveReport:

@@ -130,6 +130,11 @@ class Reference:
                                   _P(_u64), _P(ctypes.c_int)]
         L.nqref_generate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64, _P(_u64)]
         L.nqref_count_subproblems.argtypes = [ctypes.c_int, ctypes.c_int, _P(_u64)]
+        L.nqref_generate_slice.argtypes = [ctypes.c_int, ctypes.c_int, _u64, _u64, ctypes.c_void_p,
+                                           _u64, _P(_u64)]
+        L.nqref_conflict_degree.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                            _u64, ctypes.c_int, ctypes.c_int, _P(ctypes.c_int),
+                                            _P(ctypes.c_int)]
         L.nqref_write_batch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _u64, _P(_u64)]
         L.nqref_aggregate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _u64, _P(_u64)]
         L.nqref_partition.argtypes = [ctypes.c_int, _u64, ctypes.c_int, ctypes.c_void_p,
@@ -164,6 +169,24 @@ class Reference:
         t = _u64()
         self._chk(self.L.nqref_count_subproblems(n, r, ctypes.byref(t)))
         return t.value
+
+    def generate_slice(self, n, r, stride, offset=0) -> np.ndarray:
+        """Records i ≡ offset (mod stride) of the reference's own stream."""
+        total = _u64()
+        self._chk(self.L.nqref_generate_slice(n, r, stride, offset, None, 0, ctypes.byref(total)))
+        a = np.zeros(total.value, dtype=SUB_DTYPE)
+        self._chk(self.L.nqref_generate_slice(n, r, stride, offset, a.ctypes.data, total.value,
+                                              ctypes.byref(total)))
+        return a
+
+    def conflict_degree(self, addresses, width, full_warp=False, banks=32, word=4, warp=32):
+        """bankmodel.hpp:62-99 -> (transactions, max_degree)."""
+        a = np.ascontiguousarray(addresses, dtype=np.uint64)
+        t, d = ctypes.c_int(), ctypes.c_int()
+        self._chk(self.L.nqref_conflict_degree(banks, word, warp, a.ctypes.data if len(a) else None,
+                                               len(a), width, 1 if full_warp else 0,
+                                               ctypes.byref(t), ctypes.byref(d)))
+        return t.value, d.value
 
     def write_batch(self, n, r) -> str:
         ln = _u64()

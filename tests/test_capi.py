@@ -37,7 +37,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version():
-    assert _lib.lib.nq_abi_version() == 1
+    assert _lib.lib.nq_abi_version() == 2  # 2: nq_dispatch_*, solve_batch_device, span_ms
 
 
 def test_partitions_like_reference():
