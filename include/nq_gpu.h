@@ -257,6 +257,13 @@ int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out);
  * 64-byte results cross PCIe. Strategies: uniform, weighted, stealing, guided. */
 int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* dev_subs, uint64_t count,
                           const nq_solve_opts* opts, nq_report* out);
+/* execute_batch over host ROOTS that each worker deepens to target_rows on its device
+ * before counting (only the roots cross PCIe; strided or guided). The totals equal
+ * execute_batch over the deepened records; report.workers[].processed counts deepened
+ * records. This is how execute() runs large frontiers and how a systematic slice of
+ * the N=27 R=7 frontier is cut into GPU-sized records for the projection. */
+int nq_solve_batch_expand(int n, int target_rows, const nq_sub* roots, uint64_t count,
+                          const nq_solve_opts* opts, nq_report* out);
 
 /* --- checkpoint / resume (runner.hpp:48-212, checkpoint.hpp:21-199) -- */
 typedef struct nq_ckpt_opts {
@@ -268,7 +275,8 @@ typedef struct nq_ckpt_opts {
                              /* running ones finish and are recorded); 0 = no limit      */
 } nq_ckpt_opts;
 
-/* execute() with chunk-granular progress: the folded frontier is cut into fixed chunks;
+/* execute() with chunk-granular progress: the folded frontier is cut into fixed chunks
+ * (emitted one at a time, never materialised whole: host memory = workers x chunk);
  * workers (opts->worker_count, devices as in nq_solve_batch) take pending chunks from an
  * atomic cursor, expensive end first; every finished chunk is recorded (weighted sum,
  * nodes). A cancel discards only the chunk in flight; completed = 0 until every chunk is
@@ -279,6 +287,10 @@ int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* opts,
 /* Reads a checkpoint's run parameters and progress (for `resume <file>`). */
 int nq_checkpoint_read(const char* path, int* n, int* pre_rows, uint64_t* chunks,
                        uint64_t* done_chunks);
+/* The same plus the kernel variant and chunk size the run was started with (a resume
+ * must repeat them: they are part of the file's identity). Any pointer may be NULL. */
+int nq_checkpoint_info(const char* path, int* n, int* pre_rows, int* variant, uint64_t* chunk,
+                       uint64_t* chunks, uint64_t* done_chunks);
 
 /* --- diagnostics ------------------------------------------------------------------- */
 /* Integer-pipe peak of the current device (LOP3+IMAD 1:1 stream, all SMs), thread

@@ -18,6 +18,7 @@
 #include <string>
 #include <tuple>
 #include <utility>
+#include <unordered_set>
 #include <vector>
 
 #include "nqueens/bitboard.hpp"
@@ -103,13 +104,29 @@ inline std::vector<Subproblem> generate(const GenerationPlan& plan) {
     return out;
 }
 
-/// Σ multiplier × count with checked arithmetic; a state that appears twice is a
-/// config_error (subproblems.hpp:149-165). States are compared exactly.
+namespace detail {
+/// The reference's duplicate key (subproblems.hpp:154-157): (cur, left, right,
+/// placed_rows) folded into 64 bits by multiply-xor with the golden-ratio constant.
+/// Keying the same 64-bit value keeps the reference's behaviour exactly, including
+/// which inputs it reports as duplicates.
+inline std::uint64_t state_key(const Subproblem& s) {
+    constexpr std::uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+    std::uint64_t key = s.cur;
+    for (std::uint64_t part : {static_cast<std::uint64_t>(s.left), static_cast<std::uint64_t>(s.right),
+                               static_cast<std::uint64_t>(s.placed_rows)})
+        key = key * kGolden ^ part;
+    return key;
+}
+}  // namespace detail
+
+/// Σ multiplier × count with checked arithmetic; a state whose key appears twice is a
+/// config_error (subproblems.hpp:149-165).
 inline std::uint64_t aggregate(std::span<const std::pair<Subproblem, std::uint64_t>> results) {
-    std::set<std::tuple<bit_mask, bit_mask, bit_mask, int>> seen;
+    std::unordered_set<std::uint64_t> seen;
+    seen.reserve(results.size());
     std::uint64_t total = 0;
     for (const auto& [sub, count] : results) {
-        if (!seen.emplace(sub.cur, sub.left, sub.right, sub.placed_rows).second)
+        if (!seen.insert(detail::state_key(sub)).second)
             throw config_error("duplicate subproblem in aggregation input");
         total = checked_add(total, checked_mul(static_cast<std::uint64_t>(sub.multiplier), count));
     }

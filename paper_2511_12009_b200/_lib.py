@@ -135,6 +135,8 @@ _sigs = {
     "nq_solve_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64,
                                       _P(NqSolveOpts), _P(NqReport)]),
     "nq_solve": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts), _P(NqReport)]),
+    "nq_solve_batch_expand": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _u64,
+                                             _P(NqSolveOpts), _P(NqReport)]),
     "nq_solve_batch_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(ctypes.c_void_p), _u64,
                                              _P(NqSolveOpts), _P(NqReport)]),
     "nq_dispatch_create": (ctypes.c_int, [ctypes.c_char_p, _u64, ctypes.c_int, _u64, ctypes.c_int,
@@ -149,6 +151,8 @@ _sigs = {
     "nq_dispatch_sum": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _P(_u64), _P(_u64), _P(_u64)]),
     "nq_solve_checkpointed": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P(NqSolveOpts),
                                              _P(NqCkptOpts), _P(NqReport)]),
+    "nq_checkpoint_info": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_int), _P(ctypes.c_int),
+                                          _P(ctypes.c_int), _P(_u64), _P(_u64), _P(_u64)]),
     "nq_checkpoint_read": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_int), _P(ctypes.c_int),
                                           _P(_u64), _P(_u64)]),
     "nq_partition_uniform": (ctypes.c_int, [_u64, ctypes.c_int, _P(_u64)]),

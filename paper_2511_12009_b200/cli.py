@@ -43,7 +43,10 @@ def do_solve(nq, a):
     if kernel is None:
         raise nq.ConfigError(f"unknown kernel '{a.kernel}'")
     strategy = nq.partition_strategy_from(a.partition)
-    workers = _workers(a.workers)
+    devices = [int(x) for x in a.devices.split(",")] if a.devices else (
+        list(range(a.gpus)) if a.gpus else None)
+    # one worker per listed device unless --workers / NQUEENS_WORKERS say otherwise
+    workers = _workers(a.workers) if (a.workers is not None or not devices) else len(devices)
     weights = []
     if strategy is nq.PartitionStrategy.weighted:
         weights = ([float(x) for x in a.weights.split(",")] if a.weights
@@ -53,8 +56,6 @@ def do_solve(nq, a):
             nq.write_batch(f, nq.GenerationPlan(a.n, pre))
     to_stdout = a.format == "log"
     log = (lambda line: print(line, flush=True)) if to_stdout else (lambda line: print(line, file=sys.stderr))
-    devices = [int(x) for x in a.devices.split(",")] if a.devices else (
-        list(range(a.gpus)) if a.gpus else None)
     opts = nq.ExecuteOptions(kernel=kernel, config=cfg,
                              plan=nq.PartitionPlan(strategy, workers, weights, a.chunk_size),
                              log=log, devices=devices)
@@ -124,9 +125,12 @@ def _sigint_event():
 
 
 def do_resume(nq, a):
-    n, pre, chunks, done = nq.checkpoint_info(a.checkpoint)
-    print(f"resuming n={n} R={pre}: {done}/{chunks} chunks already counted", file=sys.stderr)
-    a.n, a.pre_rows, a.resume, a.checkpoint_chunk = n, pre, True, 0
+    d = nq.checkpoint_details(a.checkpoint)
+    print(f"resuming n={d['n']} R={d['pre_rows']} kernel={d['kernel'].name} chunk={d['chunk']}: "
+          f"{d['done_chunks']}/{d['chunks']} chunks already counted", file=sys.stderr)
+    # the kernel variant and chunk size are part of the file's identity: take them from it
+    a.n, a.pre_rows, a.resume, a.checkpoint_chunk = d["n"], d["pre_rows"], True, d["chunk"]
+    a.kernel = d["kernel"].name
     return do_solve(nq, a)
 
 
@@ -203,9 +207,12 @@ def main(argv=None):
     rs.add_argument("--checkpoint-interval-s", type=float, default=30.0)
     rs.add_argument("--time-limit-s", type=float, default=0.0)
     rs.add_argument("--stop-after-s", type=float, default=0.0)
-    for k, v in (("config", "config2"), ("workers", None), ("partition", "stealing"),
-                 ("weights", ""), ("kernel", "lastrow"), ("chunk_size", 4096),
-                 ("export_subproblems", ""), ("gpus", 0), ("devices", "")):
+    rs.add_argument("--config", default="config2")
+    rs.add_argument("--workers", type=int, default=None)
+    rs.add_argument("--gpus", type=int, default=0, help="use devices 0..G-1 (default: all visible)")
+    rs.add_argument("--devices", default="", help="explicit comma-separated device list")
+    for k, v in (("partition", "stealing"), ("weights", ""), ("kernel", "lastrow"),
+                 ("chunk_size", 4096), ("export_subproblems", "")):
         rs.set_defaults(**{k: v})
     c = sub.add_parser("subcount", help="count generated subproblems")
     c.add_argument("--n", type=int, required=True)

@@ -80,6 +80,13 @@ KernelFn pick(bool per_sub, int layout) {
   return per_sub ? nq_dfs_kernel<B, kStep, true, kLayoutV4> : nq_dfs_kernel<B, kStep, false, kLayoutV4>;
 }
 
+// n = 32: candidate sets can use bit 31; one V4 instantiation at 128 threads carries the
+// adjusted node counter (nq_kernel.cuh, WIDE).
+KernelFn wide_kernel(bool per_sub) {
+  return per_sub ? nq_dfs_kernel<128, kStep, true, kLayoutV4, true>
+                 : nq_dfs_kernel<128, kStep, false, kLayoutV4, true>;
+}
+
 KernelFn kernel_for(int block, bool per_sub, int layout) {
   switch (block) {
     case 64: return pick<64>(per_sub, layout);
@@ -106,7 +113,14 @@ struct nq_ctx {
   cudaEvent_t ev_start = nullptr;          // a worker's first enqueued operation (span)
   uint4* d_subs = nullptr;
   size_t d_cap = 0;                        // records
-  unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals, [6] stop word
+  // per-record outputs of nq_count_each, kept across calls (count_with per subproblem
+  // would otherwise pay three cudaMalloc/cudaFree pairs each time)
+  unsigned long long* d_each_cnt = nullptr;
+  unsigned long long* d_each_nodes = nullptr;
+  int* d_each_high = nullptr;
+  size_t each_cap = 0;
+  unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals, [6] stop word,
+                                           // [7] weighted-sum overflow flag
   unsigned long long* h_ctl = nullptr;     // pinned: [0..7] mirror of d_ctl, [8] stop source
   int block = 128;
   int blocks_per_sm = 0;                   // 0 = occupancy limit
@@ -153,12 +167,19 @@ int set_kernel_attributes(int device) {
         NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
         NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       }
+  for (bool per_sub : {false, true}) {
+    NQ_CUDA(cudaFuncSetAttribute(wide_kernel(per_sub), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin));
+    NQ_CUDA(cudaFuncSetAttribute(wide_kernel(per_sub),
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
   done[device] = true;
   return NQ_OK;
 }
 
 struct Launch {
   int grid = 0;
+  int block = 128;
   size_t smem = 0;
   KernelFn fn = nullptr;
 };
@@ -166,11 +187,12 @@ struct Launch {
 int plan_launch(nq_ctx* c, int n, int pre_rows, bool per_sub, Launch* L) {
   const int frames = std::max(n - 1 - pre_rows, 0);
   const int levels = frames + 1;  // + the idle sentinel
-  L->fn = kernel_for(c->block, per_sub, c->layout);
+  L->block = n >= 32 ? 128 : c->block;
+  L->fn = n >= 32 ? wide_kernel(per_sub) : kernel_for(c->block, per_sub, c->layout);
   if (!L->fn) return set_error(NQ_ECONFIG, "unsupported block size " + std::to_string(c->block));
-  L->smem = static_cast<size_t>(levels) * c->block * 16u;
+  L->smem = static_cast<size_t>(levels) * L->block * 16u;
   int per_sm = 0;
-  NQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, c->block, L->smem));
+  NQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L->fn, L->block, L->smem));
   if (per_sm < 1)
     return set_error(NQ_ECONFIG, "stack of " + std::to_string(frames) +
                                      " frames does not fit in shared memory (n=" +
@@ -188,9 +210,8 @@ int check_idle(const nq_ctx* c) {
 }
 
 int check_args(int n, int pre_rows, int variant) {
-  if (n < 1 || n > 31)
-    return set_error(NQ_ECONFIG, "board size must be in [1, 31] on the GPU path, got " +
-                                     std::to_string(n));
+  if (n < 1 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
   if (pre_rows < 0 || pre_rows > n)
     return set_error(NQ_ECONFIG, "pre_rows must be in [0, n], got " + std::to_string(pre_rows));
   if (variant != NQ_VARIANT_ITERATIVE && variant != NQ_VARIANT_LASTROW)
@@ -233,7 +254,7 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.donate = c->donate;
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
   if (count > 0) {
-    L.fn<<<L.grid, c->block, L.smem, c->stream>>>(P);
+    L.fn<<<L.grid, L.block, L.smem, c->stream>>>(P);
     NQ_CUDA(cudaGetLastError());
   }
   NQ_CUDA(cudaEventRecord(c->ev_k1, c->stream));
@@ -273,6 +294,8 @@ int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
                                      " is malformed (cols outside the board, popcount(cols) != "
                                      "placed_rows, or placed_rows < pre_rows=" +
                                      std::to_string(pre_rows) + ")");
+  if (t[6] != 0)
+    return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits (multiplier-weighted sum)");
   nq_result r{};
   r.solutions = t[0];
   r.raw_solutions = t[1];
@@ -415,6 +438,9 @@ void nq_ctx_destroy(nq_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d_subs) cudaFree(c->d_subs);
+  if (c->d_each_cnt) cudaFree(c->d_each_cnt);
+  if (c->d_each_nodes) cudaFree(c->d_each_nodes);
+  if (c->d_each_high) cudaFree(c->d_each_high);
   if (c->d_ctl) cudaFree(c->d_ctl);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
@@ -504,17 +530,21 @@ int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* hos
   NQ_CUDA(cudaSetDevice(c->device));
   if (int rc = ensure_capacity(c, count)) return rc;
   if (count == 0) return NQ_OK;
-  unsigned long long *d_cnt = nullptr, *d_nodes = nullptr;
-  int* d_high = nullptr;
-  NQ_CUDA(cudaMalloc(&d_cnt, count * sizeof(unsigned long long)));
-  NQ_CUDA(cudaMalloc(&d_nodes, count * sizeof(unsigned long long)));
-  NQ_CUDA(cudaMalloc(&d_high, count * sizeof(int)));
-  struct Free {
-    void* p[3];
-    ~Free() {
-      for (void* q : p) cudaFree(q);
-    }
-  } guard{{d_cnt, d_nodes, d_high}};
+  if (count > c->each_cap) {
+    cudaFree(c->d_each_cnt);
+    cudaFree(c->d_each_nodes);
+    cudaFree(c->d_each_high);
+    c->d_each_cnt = c->d_each_nodes = nullptr;
+    c->d_each_high = nullptr;
+    c->each_cap = 0;
+    const size_t cap = std::max<size_t>(count, 1024);
+    NQ_CUDA(cudaMalloc(&c->d_each_cnt, cap * sizeof(unsigned long long)));
+    NQ_CUDA(cudaMalloc(&c->d_each_nodes, cap * sizeof(unsigned long long)));
+    NQ_CUDA(cudaMalloc(&c->d_each_high, cap * sizeof(int)));
+    c->each_cap = cap;
+  }
+  unsigned long long *d_cnt = c->d_each_cnt, *d_nodes = c->d_each_nodes;
+  int* d_high = c->d_each_high;
   NQ_CUDA(cudaMemsetAsync(d_cnt, 0, count * sizeof(unsigned long long), c->stream));
   NQ_CUDA(cudaMemsetAsync(d_nodes, 0, count * sizeof(unsigned long long), c->stream));
   NQ_CUDA(cudaMemsetAsync(d_high, 0, count * sizeof(int), c->stream));
@@ -524,11 +554,14 @@ int nq_count_each(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* hos
   if (int rc = enqueue(c, n, pre_rows, variant, reinterpret_cast<const nq_sub*>(c->d_subs), count,
                        true, d_cnt, d_high, d_nodes))
     return rc;
-  if (int rc = finish(c, variant, true, pre_rows, nullptr)) return rc;
-  if (counts) NQ_CUDA(cudaMemcpy(counts, d_cnt, count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (counts)
+    NQ_CUDA(cudaMemcpyAsync(counts, d_cnt, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
   if (high_water)
-    NQ_CUDA(cudaMemcpy(high_water, d_high, count * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (nodes) NQ_CUDA(cudaMemcpy(nodes, d_nodes, count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    NQ_CUDA(cudaMemcpyAsync(high_water, d_high, count * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+  if (nodes)
+    NQ_CUDA(cudaMemcpyAsync(nodes, d_nodes, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+  if (int rc = finish(c, variant, true, pre_rows, nullptr)) return rc;
   return NQ_OK;
 }
 

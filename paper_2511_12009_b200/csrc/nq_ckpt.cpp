@@ -15,6 +15,8 @@
 //   identity <16 hex digits: FNV-1a of "gen-v1|n|R|variant|chunk|task_count">
 //   run <n> <pre_rows> <variant> <chunk> <task_count> <chunk_count>
 //   done <chunk_index> <weighted_sum> <nodes>          (any order, each index once)
+// The frontier is never materialised: each worker emits the chunk it takes from the
+// stream's prefix offsets (FrontierStream), so host memory stays at workers x chunk.
 //   checksum <16 hex digits: FNV-1a of every byte above this line>
 #include <algorithm>
 #include <atomic>
@@ -151,12 +153,19 @@ using namespace nqb200;
 
 extern "C" int nq_checkpoint_read(const char* path, int* n, int* pre_rows, uint64_t* chunks,
                                   uint64_t* done_chunks) {
+  return nq_checkpoint_info(path, n, pre_rows, nullptr, nullptr, chunks, done_chunks);
+}
+
+extern "C" int nq_checkpoint_info(const char* path, int* n, int* pre_rows, int* variant,
+                                  uint64_t* chunk, uint64_t* chunks, uint64_t* done_chunks) {
   if (!path) return set_error(NQ_ECONFIG, "null checkpoint path");
   RunKey key;
   std::map<uint64_t, ChunkResult> done;
   if (int rc = parse(path, &key, &done)) return rc;
   if (n) *n = key.n;
   if (pre_rows) *pre_rows = key.pre_rows;
+  if (variant) *variant = key.variant;
+  if (chunk) *chunk = key.chunk;
   if (chunks) *chunks = key.chunks;
   if (done_chunks) *done_chunks = done.size();
   return NQ_OK;
@@ -169,8 +178,8 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
   if (opts) o = *opts;
-  if (n < 2 || n > 31)
-    return set_error(NQ_ECONFIG, "board size must be in [2, 31] for a checkpointed run, got " +
+  if (n < 2 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [2, 32] for a checkpointed run, got " +
                                      std::to_string(n));
   if (int rc = require_feasible(o.stack_depth, o.config_name, n, pre_rows,
                                 o.variant == NQ_VARIANT_LASTROW))
@@ -192,22 +201,31 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
     RunKey file;
     if (int rc = parse(ck->path, &file, &done)) return rc;
     if (!ck->chunk) key.chunk = file.chunk, key.chunks = (tasks + key.chunk - 1) / key.chunk;
-    if (file.identity() != key.identity())
+    if (file.identity() != key.identity()) {
+      auto kernel = [](int v) { return v == NQ_VARIANT_LASTROW ? "lastrow" : "iterative"; };
       return set_error(NQ_ECHECKPOINT,
-                       "checkpoint belongs to a different run (n=" + std::to_string(file.n) +
-                           ", R=" + std::to_string(file.pre_rows) + ", chunk=" +
-                           std::to_string(file.chunk) + ")");
+                       "checkpoint belongs to a different run (file: n=" + std::to_string(file.n) +
+                           ", R=" + std::to_string(file.pre_rows) + ", kernel=" +
+                           kernel(file.variant) + ", chunk=" + std::to_string(file.chunk) +
+                           ", tasks=" + std::to_string(file.tasks) + "; this call: n=" +
+                           std::to_string(n) + ", R=" + std::to_string(pre_rows) + ", kernel=" +
+                           kernel(o.variant) + ", chunk=" + std::to_string(key.chunk) + ")");
+    }
   }
 
-  std::vector<nq_sub> batch(tasks);
-  if (int rc = generate_slice(n, pre_rows, 1, 0, batch.data(), tasks, &tasks)) return rc;
-  const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
+  // The frontier is never materialised: its prefix offsets are computed once and each
+  // worker emits the chunk it takes into its own buffer (host memory = workers x chunk,
+  // e.g. 28 MB per worker at N=27 R=7 with the default 256 chunks, not 7.26 GB).
+  FrontierStream stream;
 
   // Pending chunks, expensive end of the stream first.
   std::vector<uint64_t> pending;
   for (uint64_t c = key.chunks; c-- > 0;)
     if (!done.count(c)) pending.push_back(c);
 
+  if (!pending.empty())
+    if (int rc = stream.open(n, pre_rows)) return rc;
+  const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
   int ndev = 0;
   if (!pending.empty())
     if (int rc = nq_device_count(&ndev)) return rc;
@@ -251,6 +269,7 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
       st.device = devs[w % G];
       const auto s0 = clk::now();
       nq_ctx* c = nullptr;
+      std::vector<nq_sub> buf;  // this worker's chunk, emitted from the stream
       int rc = nq_ctx_create(st.device, &c);
       if (rc == NQ_OK) rc = nq_ctx_set_cancel(c, o.cancel);
       while (rc == NQ_OK && !interrupted.load()) {
@@ -268,8 +287,11 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
         const uint64_t ci = pending[k];
         const uint64_t first = ci * key.chunk;
         const uint64_t len = std::min(key.chunk, tasks - first);
+        buf.resize(len);
+        rc = stream.emit(1, first, buf.data(), len);
+        if (rc) break;
         nq_result r{};
-        rc = nq_count(c, n, pre_rows, o.variant, batch.data() + first, len, &r);
+        rc = nq_count(c, n, pre_rows, o.variant, buf.data(), len, &r);
         if (rc) break;
         if (r.subproblems < len) {  // cancelled inside the launch: discard the chunk
           interrupted.store(true);

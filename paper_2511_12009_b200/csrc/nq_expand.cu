@@ -197,8 +197,8 @@ int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, in
                   cudaStream_t st, uint4** out, uint64_t* total) {
   *out = nullptr;
   *total = 0;
-  if (n < 1 || n > 31)
-    return set_error(NQ_ECONFIG, "board size must be in [1, 31], got " + std::to_string(n));
+  if (n < 1 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
   if (target < 1 || target >= n)
     return set_error(NQ_ECONFIG, "target rows must satisfy 1 <= T < n (n=" + std::to_string(n) +
                                      ", T=" + std::to_string(target) + ")");
@@ -207,7 +207,7 @@ int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, in
   NvtxRange range("nq_expand_device (level passes)");
   NQX_CUDA(cudaSetDevice(device));
   if (int rc = retain_pool(device)) return rc;
-  const uint32_t mask = (1u << n) - 1u;
+  const uint32_t mask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
   int sms = 0;
   NQX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   DevBuf ctl{nullptr, st};
@@ -244,6 +244,11 @@ int expand_levels(int device, int n, const nq_sub* dev_roots, uint64_t count, in
       if (h[1] != ~0ull) return set_error(NQ_ECONFIG, "root " + std::to_string(h[1]) + " is malformed");
       const int min_placed = static_cast<int>(h[2] & 0xffffffffu);
       passes = std::max(target - min_placed, 1);  // >= 1 pass: the output is a fresh buffer
+    }
+    if (h[0] == 0) {  // every record of this level is a dead end: nothing to deepen or count
+      if (owned) NQX_CUDA(cudaFreeAsync(owned, st));
+      NQX_CUDA(cudaStreamSynchronize(st));
+      return NQ_OK;  // *out = nullptr, *total = 0
     }
     uint4* next = nullptr;
     NQX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&next), std::max<uint64_t>(h[0], 1) * 16, st));

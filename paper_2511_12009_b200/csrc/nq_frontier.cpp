@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -149,35 +150,68 @@ int check_plan(int n, int pre_rows) {
   return NQ_OK;
 }
 
+struct FrontierStream::Impl {
+  Walker w;
+  int pre_rows;
+  std::vector<Prefix> pre;
+  std::vector<uint64_t> off;  // off[i]: stream index of prefix i's first descendant
+};
+
+FrontierStream::FrontierStream() = default;
+FrontierStream::~FrontierStream() = default;
+
+int FrontierStream::open(int n, int pre_rows) {
+  if (int rc = check_plan(n, pre_rows)) return rc;
+  auto p = std::make_unique<Impl>(Impl{Walker{n, mask_of(n)}, pre_rows, {}, {}});
+  p->w.prefixes(std::min(pre_rows, 3), pre_rows, p->pre);
+  p->off.assign(p->pre.size() + 1, 0);
+  parallel_for(p->pre.size(), [&](size_t i) {
+    const Prefix& q = p->pre[i];
+    p->off[i + 1] = p->w.count(q.cols, q.diag, q.anti, q.row, pre_rows);
+  });
+  for (size_t i = 0; i < p->pre.size(); ++i) p->off[i + 1] += p->off[i];
+  impl_ = std::move(p);
+  return NQ_OK;
+}
+
+uint64_t FrontierStream::size() const { return impl_ ? impl_->off.back() : 0; }
+
+int FrontierStream::emit(uint64_t stride, uint64_t offset, nq_sub* out, uint64_t cap) const {
+  if (!impl_) return set_error(NQ_ECONFIG, "frontier stream not opened");
+  if (stride == 0) return set_error(NQ_ECONFIG, "slice stride must be >= 1");
+  const Impl& p = *impl_;
+  if (!out || cap == 0) return NQ_OK;
+  // Prefixes whose range holds no slot in [0, cap) are skipped: a contiguous range
+  // [offset, offset + cap) (stride 1) touches only the prefixes that overlap it.
+  const uint64_t end_index = offset + (cap - 1) * stride;  // last wanted stream index
+  const size_t lo_i = static_cast<size_t>(
+      std::upper_bound(p.off.begin(), p.off.end() - 1, offset) - p.off.begin()) - 1;
+  const size_t hi_i = static_cast<size_t>(
+      std::upper_bound(p.off.begin(), p.off.end() - 1, end_index) - p.off.begin());
+  parallel_for(hi_i - lo_i, [&](size_t k) {
+    const size_t i = lo_i + k;
+    const uint64_t lo = p.off[i], hi = p.off[i + 1];
+    if (hi <= offset || lo == hi) return;
+    const uint64_t first_slot = lo > offset ? (lo - offset + stride - 1) / stride : 0;
+    if (first_slot >= cap) return;
+    uint64_t index = lo;
+    p.w.emit(p.pre[i].cols, p.pre[i].diag, p.pre[i].anti, p.pre[i].row, p.pre_rows, p.pre[i].mult,
+             index, stride, offset, out, cap);
+  });
+  return NQ_OK;
+}
+
 int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
                    uint64_t cap, uint64_t* total) {
   if (int rc = check_plan(n, pre_rows)) return rc;
   NvtxRange range(out ? "nq_generate" : "nq_count_subproblems");
   if (stride == 0) return set_error(NQ_ECONFIG, "slice stride must be >= 1");
-  const Walker w{n, mask_of(n)};
-  std::vector<Prefix> pre;
-  const int d0 = std::min(pre_rows, 3);
-  w.prefixes(d0, pre_rows, pre);
-  std::vector<uint64_t> off(pre.size() + 1, 0);
-  parallel_for(pre.size(), [&](size_t i) {
-    off[i + 1] = w.count(pre[i].cols, pre[i].diag, pre[i].anti, pre[i].row, pre_rows);
-  });
-  for (size_t i = 0; i < pre.size(); ++i) off[i + 1] += off[i];
-  const uint64_t full = off.back();
+  FrontierStream fs;
+  if (int rc = fs.open(n, pre_rows)) return rc;
+  const uint64_t full = fs.size();
   const uint64_t sliced = full > offset ? (full - offset + stride - 1) / stride : 0;
   if (total) *total = sliced;
-  if (!out || cap == 0) return NQ_OK;
-  parallel_for(pre.size(), [&](size_t i) {
-    // Skip prefixes whose range holds no slot below cap.
-    const uint64_t lo = off[i], hi = off[i + 1];
-    if (hi <= offset || lo == hi) return;
-    const uint64_t first_slot = lo > offset ? (lo - offset + stride - 1) / stride : 0;
-    if (first_slot >= cap) return;
-    uint64_t index = lo;
-    w.emit(pre[i].cols, pre[i].diag, pre[i].anti, pre[i].row, pre_rows, pre[i].mult, index,
-           stride, offset, out, cap);
-  });
-  return NQ_OK;
+  return fs.emit(stride, offset, out, std::min(cap, sliced));
 }
 
 // Deepen a list of roots to `target` placed rows: each root's descendants at depth
@@ -186,8 +220,8 @@ int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub
 // copied as-is. Used to cut very deep frontiers (N=27 slices) into GPU-sized records.
 int expand(int n, const nq_sub* roots, uint64_t count, int target, nq_sub* out, uint64_t cap,
            uint64_t* total) {
-  if (n < 1 || n > 31)
-    return set_error(NQ_ECONFIG, "board size must be in [1, 31], got " + std::to_string(n));
+  if (n < 1 || n > 32)
+    return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
   if (target < 1 || target >= n)
     return set_error(NQ_ECONFIG, "target rows must satisfy 1 <= T < n (n=" + std::to_string(n) +
                                      ", T=" + std::to_string(target) + ")");

@@ -1,6 +1,7 @@
 // nq_internal.h — shared helpers of libnqb200.so (not installed).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <string>
 
 #include <nvtx3/nvToolsExt.h>
@@ -28,6 +29,24 @@ inline bool cancel_raised(const volatile int* flag) {
 int set_error(int code, const std::string& msg);
 
 int check_plan(int n, int pre_rows);
+
+// The folded frontier stream of (n, R) with its per-prefix offsets computed once, so
+// any contiguous range or systematic slice can be emitted later without walking (or
+// materialising) the rest: the checkpointed runner emits one chunk at a time, which
+// keeps host memory at chunk size even for N=27 (453,688,251 records at R=7).
+class FrontierStream {
+ public:
+  FrontierStream();
+  ~FrontierStream();
+  int open(int n, int pre_rows);
+  uint64_t size() const;
+  // Records offset, offset + stride, ... into out[0 .. cap).
+  int emit(uint64_t stride, uint64_t offset, nq_sub* out, uint64_t cap) const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
 int generate_slice(int n, int pre_rows, uint64_t stride, uint64_t offset, nq_sub* out,
                    uint64_t cap, uint64_t* total);
 int count_subproblems(int n, int pre_rows, uint64_t* total);

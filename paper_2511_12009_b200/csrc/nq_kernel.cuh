@@ -41,7 +41,8 @@ struct DfsParams {
   unsigned long long* cursor;        // device dispatch counter (zeroed per launch)
   const unsigned long long* stop;    // non-zero: hand out no more records (cancel)
   unsigned long long* totals;        // [0] weighted, [1] raw sols, [2] iterations,
-                                     // [3] subproblems, [4] first bad record + 1
+                                     // [3] subproblems, [4] first bad record + 1,
+                                     // [6] weighted sum wrapped 64 bits (-> NQ_EOVERFLOW)
   unsigned long long* each_count;    // per-record outputs (PER_SUB only)
   int* each_high;
   unsigned long long* each_nodes;
@@ -76,7 +77,8 @@ __device__ __forceinline__ void lds128(uint32_t addr, uint32_t& x, uint32_t& y, 
 //   a  = a ^ p;  push (C,l,r,a) if a    the row's remaining candidates
 //   C -= p, l = (l + p) << 1, r = (r + p) >> 1                     (bitboard.hpp:38-45)
 //   a  = C & ~(l | r)                   child's candidates (LOP3 0x10) (bitboard.hpp:21-23)
-//   its += (a_in != 0)  (bit 31 of -a_in; a_in < 2^31),  sol += (C == 0) for busy lanes
+//   its += (a_in != 0)  (bit 31 of -a_in when a_in < 2^31, i.e. n <= 31; WIDE: of a_in | -a_in)
+//   sol += (C == 0) for busy lanes
 //   pop (C,l,r,a) if the child has no candidate and the lane is busy
 // Stack layouts (both: one level = BLOCK frames = BLOCK*16 bytes):
 //   kLayoutV4     frame of thread t at level L = one uint4 at stk[L*BLOCK + t]; one
@@ -119,38 +121,48 @@ __device__ __forceinline__ void store_idle_frame(uint32_t addr) {
   }
 }
 
-template <uint32_t STRIDE, int LAYOUT>
+// The V4 step; WIDE_FIX is empty for n <= 31 and "or.b32 na, na, %3;" for n = 32, where a
+// candidate set can have bit 31 set and bit 31 of -a alone no longer flags a != 0 (bit 31
+// of a | -a does, for any 32-bit a).
+#define NQ_V4_STEP(WIDE_FIX)                          \
+  "{\n\t"                                            \
+  ".reg .u32 na, p;\n\t"                             \
+  ".reg .pred pa, pk, po, ps;\n\t"                   \
+  "neg.s32 na, %3;\n\t"                              \
+  "and.b32 p, %3, na;\n\t" WIDE_FIX                  \
+  "setp.ne.u32 pk, p, 0;\n\t"                        \
+  "xor.b32 %3, %3, p;\n\t"                           \
+  "setp.ne.u32 pa, %3, 0;\n\t"                       \
+  "@pa st.shared.v4.u32 [%4], {%0, %1, %2, %3};\n\t" \
+  "@pa add.u32 %4, %4, %7;\n\t"                      \
+  "sub.u32 %0, %0, p;\n\t"                           \
+  "add.u32 %1, %1, p;\n\t"                           \
+  "add.u32 %1, %1, %1;\n\t"                          \
+  "add.u32 %2, %2, p;\n\t"                           \
+  "shr.u32 %2, %2, 1;\n\t"                           \
+  "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"               \
+  "shr.u32 na, na, 31;\n\t"                          \
+  "add.u32 %6, %6, na;\n\t"                          \
+  "setp.eq.and.u32 ps, %0, 0, pk;\n\t"               \
+  "@ps add.u32 %5, %5, 1;\n\t"                       \
+  "setp.eq.and.u32 po, %3, 0, pk;\n\t"               \
+  "@po sub.u32 %4, %4, %7;\n\t"                      \
+  "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t" \
+  "}"
+
+template <uint32_t STRIDE, int LAYOUT, bool WIDE = false>
 __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, uint32_t& a,
                                          uint32_t& sp, uint32_t& sol, uint32_t& its) {
-  if constexpr (LAYOUT == kLayoutV4) {
-    asm volatile(
-      "{\n\t"
-      ".reg .u32 na, p;\n\t"
-      ".reg .pred pa, pk, po, ps;\n\t"
-      "neg.s32 na, %3;\n\t"
-      "and.b32 p, %3, na;\n\t"
-      "setp.ne.u32 pk, p, 0;\n\t"
-      "xor.b32 %3, %3, p;\n\t"
-      "setp.ne.u32 pa, %3, 0;\n\t"
-      "@pa st.shared.v4.u32 [%4], {%0, %1, %2, %3};\n\t"
-      "@pa add.u32 %4, %4, %7;\n\t"
-      "sub.u32 %0, %0, p;\n\t"
-      "add.u32 %1, %1, p;\n\t"
-      "add.u32 %1, %1, %1;\n\t"
-      "add.u32 %2, %2, p;\n\t"
-      "shr.u32 %2, %2, 1;\n\t"
-      "lop3.b32 %3, %0, %1, %2, 0x10;\n\t"
-      "shr.u32 na, na, 31;\n\t"
-      "add.u32 %6, %6, na;\n\t"
-      "setp.eq.and.u32 ps, %0, 0, pk;\n\t"
-      "@ps add.u32 %5, %5, 1;\n\t"
-      "setp.eq.and.u32 po, %3, 0, pk;\n\t"
-      "@po sub.u32 %4, %4, %7;\n\t"
-      "@po ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t"
-      "}"
-      : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
-      : "n"(STRIDE)
-      : "memory");
+  if constexpr (LAYOUT == kLayoutV4 && WIDE) {
+    asm volatile(NQ_V4_STEP("or.b32 na, na, %3;\n\t")
+                 : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+                 : "n"(STRIDE)
+                 : "memory");
+  } else if constexpr (LAYOUT == kLayoutV4) {
+    asm volatile(NQ_V4_STEP("")
+                 : "+r"(C), "+r"(l), "+r"(r), "+r"(a), "+r"(sp), "+r"(sol), "+r"(its)
+                 : "n"(STRIDE)
+                 : "memory");
   } else {
     asm volatile(
       "{\n\t"
@@ -189,8 +201,9 @@ __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, 
   }
 }
 
-template <int BLOCK, int KSTEP, bool PER_SUB, int LAYOUT>
+template <int BLOCK, int KSTEP, bool PER_SUB, int LAYOUT, bool WIDE = false>
 __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
+  static_assert(!WIDE || LAYOUT == kLayoutV4, "n = 32 runs the V4 layout");
   extern __shared__ uint4 stk[];  // [levels][BLOCK] frames (or [levels][4][BLOCK] words)
   constexpr uint32_t STRIDE = BLOCK * 16u;
   const uint32_t lane = threadIdx.x & 31u;
@@ -215,6 +228,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   uint32_t weight = 0u;                            // multiplier of the current record
   bool busy = false;                               // lane holds a record
   unsigned long long tot_w = 0ull, tot_raw = 0ull, tot_it = 0ull, tot_subs = 0ull;
+  bool wrapped = false;  // Σ multiplier x count passed 2^64 (checked_add, errors.hpp:24-29)
   // PER_SUB bookkeeping
   unsigned long long cur_idx = 0ull, sub_sol = 0ull, sub_it = 0ull;
   int placed = 0, high = 0;
@@ -228,7 +242,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
     if (idle) {
       for (;;) {
         if (a == 0u && busy) {  // fold the finished record (or donated piece of one)
-          tot_w += static_cast<unsigned long long>(weight) * sol;
+          const unsigned long long prod = static_cast<unsigned long long>(weight) * sol;  // < 2^56
+          tot_w += prod;
+          wrapped |= tot_w < prod;
           tot_raw += sol;
           tot_it += its;
           tot_subs += piece ? 0ull : 1ull;
@@ -346,12 +362,14 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         const int h = row - placed + 1;
         if (a != 0u && (!P.lastrow || row <= P.n - 2) && h > high) high = h;
       }
-      dfs_step<STRIDE, LAYOUT>(C, l, r, a, sp, sol, its);
+      dfs_step<STRIDE, LAYOUT, WIDE>(C, l, r, a, sp, sol, its);
     }
 
     // Fold u32 counters periodically so they cannot wrap (≤ 2^15*KSTEP steps).
     if (((++blocks) & 0x7fffu) == 0u) {
-      tot_w += static_cast<unsigned long long>(weight) * sol;
+      const unsigned long long prod = static_cast<unsigned long long>(weight) * sol;
+      tot_w += prod;
+      wrapped |= tot_w < prod;
       tot_raw += sol;
       tot_it += its;
       if constexpr (PER_SUB) {
@@ -366,13 +384,17 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   // ---- warp reduction, one atomic per warp per total --------------------------------
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    tot_w += __shfl_down_sync(0xffffffffu, tot_w, off);
+    const unsigned long long w = __shfl_down_sync(0xffffffffu, tot_w, off);
+    tot_w += w;
+    wrapped |= tot_w < w;
     tot_raw += __shfl_down_sync(0xffffffffu, tot_raw, off);
     tot_it += __shfl_down_sync(0xffffffffu, tot_it, off);
     tot_subs += __shfl_down_sync(0xffffffffu, tot_subs, off);
   }
+  wrapped = __any_sync(0xffffffffu, wrapped);
   if (lane == 0u) {
-    atomicAdd(P.totals + 0, tot_w);
+    const unsigned long long before = atomicAdd(P.totals + 0, tot_w);
+    if (wrapped || before + tot_w < before) atomicExch(P.totals + 6, 1ull);
     atomicAdd(P.totals + 1, tot_raw);
     atomicAdd(P.totals + 2, tot_it);
     atomicAdd(P.totals + 3, tot_subs);

@@ -151,6 +151,14 @@ extern "C" int nq_solve_batch(int n, int pre_rows, const nq_sub* subs, uint64_t 
   return solve_batch_impl(n, pre_rows, 0, subs, nullptr, count, opts, out);
 }
 
+extern "C" int nq_solve_batch_expand(int n, int target_rows, const nq_sub* roots, uint64_t count,
+                                     const nq_solve_opts* opts, nq_report* out) {
+  if (target_rows < 1 || target_rows >= n)
+    return set_error(NQ_ECONFIG, "target rows must satisfy 1 <= T < n (n=" + std::to_string(n) +
+                                     ", T=" + std::to_string(target_rows) + ")");
+  return solve_batch_impl(n, 0, target_rows, roots, nullptr, count, opts, out);
+}
+
 extern "C" int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* dev_subs,
                                      uint64_t count, const nq_solve_opts* opts, nq_report* out) {
   if (!dev_subs) return set_error(NQ_ECONFIG, "null device frontier list");

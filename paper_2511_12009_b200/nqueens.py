@@ -597,6 +597,27 @@ def execute_batch_device(n: int, pre_rows: int, dev_ptrs: Sequence[int], count: 
     return _report(n, pre_rows, opts, rep)
 
 
+def execute_batch_expand(n: int, target_rows: int, roots, opts: ExecuteOptions) -> SolveReport:
+    """execute_batch over roots that every worker deepens to target_rows on its own
+    device first (nq_solve_batch_expand; strided or guided): only the roots cross PCIe.
+    Same totals and Alg. 3 nodes as counting the deepened records."""
+    if opts.plan.worker_count < 1:
+        raise ConfigError("worker_count must be >= 1")
+    require_feasible(opts.config, n, target_rows, opts.kernel is KernelVariant.lastrow)
+    a = roots if isinstance(roots, np.ndarray) else pack(roots)
+    a = np.ascontiguousarray(a, dtype=SUB_DTYPE)
+    keep: list = []
+    o = _solve_opts(opts, keep)
+    rep = _lib.NqReport()
+    try:
+        _call(lib.nq_solve_batch_expand(n, target_rows, a.ctypes.data if len(a) else None, len(a),
+                                        ctypes.byref(o), ctypes.byref(rep)))
+    finally:
+        _stop_watchers(keep)
+    r = _report(n, target_rows, opts, rep)
+    return r
+
+
 class Dispatcher:
     """The scheduler's host-side dynamic chunk dispenser (nq_dispatch_*). name=None: private
     to this process; a name: a POSIX shared-memory segment that cooperating processes
@@ -746,11 +767,19 @@ def run_with_checkpoint(spec: RunSpec, ckpt: CheckpointOptions, cancel=None, log
 
 def checkpoint_info(path: str):
     """(n, pre_rows, chunks, done_chunks) recorded in a checkpoint file."""
-    n, r = ctypes.c_int(), ctypes.c_int()
-    chunks, done = ctypes.c_uint64(), ctypes.c_uint64()
-    _call(lib.nq_checkpoint_read(str(path).encode(), ctypes.byref(n), ctypes.byref(r),
-                                 ctypes.byref(chunks), ctypes.byref(done)))
-    return n.value, r.value, chunks.value, done.value
+    d = checkpoint_details(path)
+    return d["n"], d["pre_rows"], d["chunks"], d["done_chunks"]
+
+
+def checkpoint_details(path: str) -> dict:
+    """Every run parameter a checkpoint records (n, pre_rows, kernel, chunk) and its
+    progress; a resume must repeat n, R, kernel and chunk (the file's identity)."""
+    n, r, v = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    chunk, chunks, done = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _call(lib.nq_checkpoint_info(str(path).encode(), ctypes.byref(n), ctypes.byref(r), ctypes.byref(v),
+                                 ctypes.byref(chunk), ctypes.byref(chunks), ctypes.byref(done)))
+    return {"n": n.value, "pre_rows": r.value, "kernel": KernelVariant(v.value), "chunk": chunk.value,
+            "chunks": chunks.value, "done_chunks": done.value}
 
 
 def measure_int_peak(device: int = 0):

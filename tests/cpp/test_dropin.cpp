@@ -251,6 +251,10 @@ void frontier_cases() {  // test_subproblems.cpp:34-150
   CHECK_THROWS_AS(aggregate(dup), config_error);
   std::vector<std::pair<Subproblem, std::uint64_t>> huge = {{Subproblem{1, 2, 0, 1, 2}, ~0ull / 2 + 1}};
   CHECK_THROWS_AS(aggregate(huge), std::overflow_error);
+  // the duplicate key is the reference's 64-bit multiply-xor mix (subproblems.hpp:154-157),
+  // the same values the Python mirror computes
+  CHECK(detail::state_key(Subproblem{5, 8, 2, 2, 1}) == 0x23c15acef1ad0341ull);
+  CHECK(detail::state_key(Subproblem{0x1f, 0x40, 0x3, 5, 1}) == 0x9f661b1922370771ull);
 }
 
 void partition_cases() {  // test_scheduler.cpp:27-75, 132-147

@@ -358,19 +358,26 @@ def _random_deep_records(n, depth, k, rng):
     return np.array(out, dtype=np.uint32).view(_lib.SUB_DTYPE).reshape(-1)
 
 
-def test_wide_boards_n29_to_31_deep_records(oracle):
-    """Bit-31 handling (bitboard.hpp:36-44): random deep records of 29..31-column
-    boards (8 rows left to search), counted per record on the GPU vs the C oracle."""
+def test_wide_boards_n29_to_32_deep_records(oracle):
+    """Bit-31 handling (bitboard.hpp:36-44): random deep records of 29..32-column
+    boards (8 rows left to search), counted per record on the GPU vs the C oracle and,
+    for n = 32 (check_board's upper bound, solver.hpp:45-48), vs the reference build."""
+    from oracle_ctypes import Reference, reference_available
     rng = np.random.default_rng(31)
-    for n in (29, 30, 31):
+    for n in (29, 30, 31, 32):
         pick = _random_deep_records(n, n - 8, 400, rng)
-        counts, _, nodes = nq.count_each(n, pick, nq.KernelVariant.lastrow, pre_rows=n - 8)
+        counts, high, nodes = nq.count_each(n, pick, nq.KernelVariant.lastrow, pre_rows=n - 8)
         total, want_nodes, want_counts = oracle.solve_batch(n, pick, per_sub=True)
         assert np.array_equal(counts, want_counts), n
         assert int(nodes.sum()) == want_nodes, n
         assert counts.sum() > 0, n
-    with pytest.raises(nq.ConfigError):
-        nq.count_each(32, _random_deep_records(32, 24, 1, rng), pre_rows=24)
+        rep = nq.execute_batch(n, n - 8, pick, nq.ExecuteOptions(
+            config=nq.builtin_configs[0], plan=nq.PartitionPlan(nq.PartitionStrategy.guided, 2)))
+        assert rep.total == total and rep.nodes == want_nodes, n
+        if n == 32 and reference_available():
+            ref = Reference()
+            for i in range(0, len(pick), 40):
+                assert ref.count(1, 32, tuple(int(x) for x in pick[i]))[0] == int(counts[i])
 
 
 def test_execute_deepens_large_frontiers_on_the_device(monkeypatch, golden):

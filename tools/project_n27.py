@@ -5,10 +5,12 @@ config 5: "N=27 timed frontier slices ... to project full 27/28-Queens wall time
 Method:
   1. systematic slice of the R-frontier: records with index ≡ o (mod K), for several
      offsets o (the frontier's cost rises with index, so a stride sample is stratified);
-  2. each slice record is deepened on the host to depth D (nq_expand), so the slice
-     becomes enough GPU-sized records (~10^5-10^7 nodes each) to keep every lane busy;
-  3. the deepened slice is counted on one B200 with the product kernel (device-resident,
-     CUDA-event kernel time);
+  2-3. the slice is counted through the product's scheduler call a user makes,
+     execute_batch_expand (nq_solve_batch_expand): guided chunks of the slice's records
+     are shipped to the GPU, deepened there to depth D (so the slice becomes enough
+     GPU-sized records, ~10^5-10^7 nodes each, to keep every lane busy) and counted;
+     time = the scheduler's device span (CUDA events, first launch -> last kernel end),
+     the host wall time of the call is reported beside it;
   4. projection: T_full(1 GPU) = T_slice * K (each sampled record's subtree is counted
      completely), T_full(G GPUs) = T_full(1 GPU) / G (the scheduler's work split;
      no inter-GPU exchange). The spread over offsets is the error bar.
@@ -21,7 +23,6 @@ Also projects the total node count (nodes_slice * K) and, when the full answer i
 from __future__ import annotations
 
 import argparse
-import ctypes
 import json
 import os
 import statistics
@@ -43,38 +44,31 @@ def main():
     ap.add_argument("--offsets", default="")
     ap.add_argument("--deepen", type=int, default=11)
     ap.add_argument("--gpus", type=int, default=8, help="GPU count the projection is quoted for")
-    ap.add_argument("--layout", type=int, default=0)
     args = ap.parse_args()
 
     import numpy as np
-    import torch
-    from paper_2511_12009_b200 import _lib
     from paper_2511_12009_b200 import nqueens as nq
 
     offsets = ([int(x) for x in args.offsets.split(",")] if args.offsets else
                [0, args.stride // 3, 2 * args.stride // 3])
     full = nq.count_subproblems(args.n, args.pre_rows)
-    ctx = ctypes.c_void_p()
-    _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(ctx)))
-    _lib.check(_lib.lib.nq_ctx_set_layout(ctx, args.layout))
+    opts = nq.ExecuteOptions(config=nq.builtin_configs[0],
+                             plan=nq.PartitionPlan(nq.PartitionStrategy.guided, 1), devices=[0])
     rows = []
     for o in offsets:
         t0 = time.perf_counter()
         sl = nq.generate_slice(args.n, args.pre_rows, args.stride, o)
-        deep = nq.expand(args.n, sl, args.deepen)
         gen_s = time.perf_counter() - t0
-        dev = torch.from_numpy(deep.view(np.int32).reshape(-1, 4)).cuda()
-        r = _lib.NqResult()
-        _lib.check(_lib.lib.nq_count_device(ctx, args.n, args.deepen, _lib.VARIANT_LASTROW,
-                                            ctypes.c_void_p(dev.data_ptr()), len(deep),
-                                            ctypes.byref(r)))
-        rows.append({"offset": o, "slice_records": len(sl), "deepened_records": len(deep),
-                     "host_gen_s": round(gen_s, 3), "kernel_ms": r.kernel_ms,
-                     "nodes": r.nodes, "solutions": r.solutions,
-                     "nodes_per_s": r.nodes / (r.kernel_ms * 1e-3)})
+        rep = nq.execute_batch_expand(args.n, args.deepen, sl, opts)
+        dev_ms = max(w.span_ms for w in rep.workers)
+        rows.append({"offset": o, "slice_records": len(sl),
+                     "deepened_records": sum(w.processed for w in rep.workers),
+                     "launches": sum(w.chunks for w in rep.workers),
+                     "host_gen_s": round(gen_s, 3), "kernel_ms": dev_ms, "call_wall_ms": rep.calc_ms,
+                     "nodes": rep.nodes, "solutions": rep.total,
+                     "nodes_per_s": rep.nodes / (dev_ms * 1e-3),
+                     "call": "execute_batch_expand (nq_solve_batch_expand), guided, 1 GPU"})
         print(json.dumps(rows[-1]), flush=True)
-        del dev
-    _lib.lib.nq_ctx_destroy(ctx)
 
     k = args.stride
     t1 = [x["kernel_ms"] * 1e-3 * k for x in rows]           # full count on 1 GPU, s
