@@ -355,7 +355,7 @@ def run_single_process(args):
                                                 ctypes.byref(r)))
             return r.kernel_ms, r.nodes, r.solutions, 1
         rep = sched.device_resident([d.data_ptr() for d in devs], count)
-        return span_ms(rep), rep.nodes, rep.total, sum(w.chunks for w in workers_of(rep))
+        return span_ms(rep), rep.nodes, rep.total, sum(w.launches for w in workers_of(rep))
 
     def flush_l2():
         for f in flush:
@@ -403,8 +403,8 @@ def run_single_process(args):
             wall.append((time.perf_counter() - t0) * 1e3)
             check_total(args.n, rep.total, "e2e step")
         line["e2e"] = {"value": nodes_per_step * args.steps / (sum(wall) / 1e3), "unit": "nodes/s",
-                       "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": 64 * sum(
-                           w.chunks for w in workers_of(rep)),
+                       "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": 80 * sum(
+                           w.launches for w in workers_of(rep)),
                        "ms_per_step": sum(wall) / args.steps,
                        "call": f"nq_solve_batch (execute_batch) on the pinned host frontier, "
                                f"{args.dispatch} dispatch over {G} GPU(s); every chunk H2D by the "
@@ -517,7 +517,7 @@ def run_torchrun(args):
         torch.cuda.synchronize()
         rep, summed = one_pass(dev_pass)
         spans.append(span_ms(rep) if rep.worker_count else 0.0)
-        launches += sum(w.chunks for w in workers_of(rep))
+        launches += sum(w.launches for w in workers_of(rep))
         if rank == 0:
             check_total(args.n, summed[0], "device-resident step")
             if summed[2] != count:
@@ -547,7 +547,7 @@ def run_torchrun(args):
                 check_total(args.n, summed[0], "e2e step")
         w = torch.tensor(wall, dtype=torch.float64)
         dist.all_reduce(w, op=dist.ReduceOp.MAX)
-        nl = torch.tensor([float(sum(x.chunks for x in workers_of(rep)))], dtype=torch.float64)
+        nl = torch.tensor([float(sum(x.launches for x in workers_of(rep)))], dtype=torch.float64)
         dist.all_reduce(nl, op=dist.ReduceOp.SUM)
         e2e = (w.tolist(), int(nl.item()))
     if rank == 0:
@@ -564,7 +564,7 @@ def run_torchrun(args):
         if e2e is not None:
             line["e2e"] = {"value": nodes_per_step * args.steps / (sum(e2e[0]) / 1e3),
                            "unit": "nodes/s", "h2d_bytes_per_step": count * 16,
-                           "d2h_bytes_per_step": 64 * e2e[1],
+                           "d2h_bytes_per_step": 80 * e2e[1],
                            "ms_per_step": sum(e2e[0]) / args.steps,
                            "call": "nq_solve_batch per rank on the pinned host frontier, chunks "
                                    "from the shared dispenser, H2D by the GPU that takes them; "

@@ -158,9 +158,9 @@ int nq_partition_weighted(uint64_t task_count, const double* weights, int worker
 
 /* --- multi-GPU execution (scheduler.hpp:266 / :573) --------------------------------
  * One host thread per worker; worker w runs on devices[w % G] with its own pooled
- * contexts (workers that share a device get distinct ones). The dynamic strategies keep
- * two launches in flight per worker on two streams, so the next chunk's blocks fill the
- * SMs the previous chunk's tail frees. */
+ * context (workers that share a device get distinct ones). Under the dynamic strategies
+ * each worker runs ONE persistent streaming launch and publishes the chunks it takes
+ * from the dispenser into it while it runs: no launch or end-of-launch tail per chunk. */
 #define NQ_PARTITION_UNIFORM 0  /* PartitionStrategy::uniform  (scheduler.hpp:26)        */
 #define NQ_PARTITION_WEIGHTED 1 /* PartitionStrategy::weighted                          */
 #define NQ_PARTITION_STEALING 2 /* PartitionStrategy::stealing: fixed chunks, cursor    */
@@ -230,11 +230,13 @@ typedef struct nq_worker_stats {
   uint64_t processed;          /* records counted by this worker                        */
   uint64_t partial_sum;        /* multiplier-weighted (checked)                         */
   uint64_t nodes;              /* Alg. 3 nodes                                          */
-  uint64_t chunks;             /* kernel launches                                       */
+  uint64_t chunks;             /* chunks / ranges counted                               */
   double elapsed_ms;           /* host wall time of this worker thread                  */
   double kernel_ms;            /* Σ device time of its launches (they may overlap)      */
   double span_ms;              /* device time from its first enqueued operation to the  */
                                /* end of its last kernel (CUDA events, one device)       */
+  uint64_t launches;           /* kernel launches (dynamic strategies: one streaming    */
+                               /* launch fed all of the worker's chunks)                 */
 } nq_worker_stats;
 
 typedef struct nq_report {

@@ -356,7 +356,7 @@ inline SolveReport to_report(int n, int pre_rows, const ExecuteOptions& opts,
         d.elapsed_ms = s.elapsed_ms;
         d.device = s.device;
         d.nodes = s.nodes;
-        d.launches = s.chunks;
+        d.launches = s.launches;
         d.kernel_ms = s.kernel_ms;
         d.span_ms = s.span_ms;
         if (opts.progress && s.assigned)
@@ -426,7 +426,7 @@ inline SolveReport execute_checkpointed(int n, int pre_rows, const ExecuteOption
         d.elapsed_ms = rep.workers[w].elapsed_ms;
         d.device = rep.workers[w].device;
         d.nodes = rep.workers[w].nodes;
-        d.launches = rep.workers[w].chunks;
+        d.launches = rep.workers[w].launches;
         d.kernel_ms = rep.workers[w].kernel_ms;
         d.span_ms = rep.workers[w].span_ms;
         report.workers.push_back(d);

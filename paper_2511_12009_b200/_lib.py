@@ -62,7 +62,8 @@ class NqWorkerStats(ctypes.Structure):
                 ("assigned", ctypes.c_uint64), ("processed", ctypes.c_uint64),
                 ("partial_sum", ctypes.c_uint64), ("nodes", ctypes.c_uint64),
                 ("chunks", ctypes.c_uint64), ("elapsed_ms", ctypes.c_double),
-                ("kernel_ms", ctypes.c_double), ("span_ms", ctypes.c_double)]
+                ("kernel_ms", ctypes.c_double), ("span_ms", ctypes.c_double),
+                ("launches", ctypes.c_uint64)]
 
 
 class NqReport(ctypes.Structure):

@@ -119,9 +119,11 @@ struct nq_ctx {
   unsigned long long* d_each_nodes = nullptr;
   int* d_each_high = nullptr;
   size_t each_cap = 0;
-  unsigned long long* d_ctl = nullptr;     // [0] cursor, [1..5] totals, [6] stop word,
-                                           // [7] weighted-sum overflow flag
-  unsigned long long* h_ctl = nullptr;     // pinned: [0..7] mirror of d_ctl, [8] stop source
+  // [0] cursor, [1..5] totals, [6] stop word, [7] weighted-sum overflow flag,
+  // [8] streaming watchdog flag, [9] streaming publish word (count | closed << 63)
+  unsigned long long* d_ctl = nullptr;
+  // pinned: [0..9] mirror of d_ctl, [10] stop source, [11] publish staging, [12] cursor read
+  unsigned long long* h_ctl = nullptr;
   int block = 128;
   int blocks_per_sm = 0;                   // 0 = occupancy limit
   int reverse = 1;
@@ -135,6 +137,13 @@ struct nq_ctx {
   uint64_t p_count = 0;
   uint64_t last_bad = ~0ull;               // index (within the batch) of a rejected record
   uint64_t last_expanded = 0;              // records produced by the last nq_count_expand
+  // streaming launch (ctx_stream_*): the chunk table the host appends to while it runs
+  QChunk* d_tab = nullptr;
+  QChunk* h_tab = nullptr;                 // pinned staging of the same entries
+  uint64_t tab_cap = 0, tab_n = 0;
+  uint64_t published = 0;
+  bool stream_open = false;
+  std::vector<void*> stream_bufs;          // deepened chunks, released after the launch
 };
 
 namespace nqb200 {
@@ -236,7 +245,8 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
             unsigned long long* each_nodes) {
   Launch L;
   if (int rc = plan_launch(c, n, pre_rows, per_sub, &L)) return rc;
-  NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 8 * sizeof(unsigned long long), c->stream));
+  if (!c->stream_open)
+    NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 10 * sizeof(unsigned long long), c->stream));
   DfsParams P{};
   P.subs = reinterpret_cast<const uint4*>(dev_subs);
   P.count = count;
@@ -252,13 +262,16 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.reverse = c->reverse;
   P.lastrow = variant == NQ_VARIANT_LASTROW;
   P.donate = c->donate;
+  P.stream = c->stream_open ? 1 : 0;
+  P.q_tab = c->d_tab;
+  P.q_pub = c->d_ctl + 9;
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
-  if (count > 0) {
+  if (count > 0 || c->stream_open) {
     L.fn<<<L.grid, L.block, L.smem, c->stream>>>(P);
     NQ_CUDA(cudaGetLastError());
   }
   NQ_CUDA(cudaEventRecord(c->ev_k1, c->stream));
-  NQ_CUDA(cudaMemcpyAsync(c->h_ctl, c->d_ctl, 8 * sizeof(unsigned long long),
+  NQ_CUDA(cudaMemcpyAsync(c->h_ctl, c->d_ctl, 10 * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, c->stream));
   return NQ_OK;
 }
@@ -274,8 +287,8 @@ int wait_for(nq_ctx* c) {
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) NQ_CUDA(q);
     if (!sent && cancel_raised(c->cancel)) {  // raise the device stop word behind the running kernel
-      c->h_ctl[8] = 1;
-      NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 8, sizeof(unsigned long long),
+      c->h_ctl[10] = 1;
+      NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 10, sizeof(unsigned long long),
                               cudaMemcpyHostToDevice, c->side));
       sent = true;
     }
@@ -296,6 +309,10 @@ int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
                                      std::to_string(pre_rows) + ")");
   if (t[6] != 0)
     return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits (multiplier-weighted sum)");
+  if (t[7] != 0)
+    return set_error(NQ_ECUDA, "streaming launch: no chunk was published for " +
+                                   std::to_string(kQueueWatchdogNs / 1000000000ull) +
+                                   " s (host side stalled); the launch gave up");
   nq_result r{};
   r.solutions = t[0];
   r.raw_solutions = t[1];
@@ -374,6 +391,124 @@ int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, 
   return NQ_OK;
 }
 
+// ---- streaming launch --------------------------------------------------------------------
+int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks, uint64_t host_records) {
+  if (!c) return set_error(NQ_ECONFIG, "null context");
+  if (c->pending) return set_error(NQ_ECONFIG, "a batch is already in flight on this context");
+  NQ_CUDA(cudaSetDevice(c->device));
+  if (max_chunks > c->tab_cap) {
+    if (c->d_tab) cudaFree(c->d_tab);
+    if (c->h_tab) cudaFreeHost(c->h_tab);
+    c->d_tab = nullptr;
+    c->h_tab = nullptr;
+    c->tab_cap = 0;
+    NQ_CUDA(cudaMalloc(&c->d_tab, max_chunks * sizeof(QChunk)));
+    NQ_CUDA(cudaMallocHost(&c->h_tab, max_chunks * sizeof(QChunk)));
+    c->tab_cap = max_chunks;
+  }
+  if (host_records)
+    if (int rc = ensure_capacity(c, host_records)) return rc;
+  // The reset must land before the first publish (side stream): wait for it here.
+  NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 10 * sizeof(unsigned long long), c->stream));
+  NQ_CUDA(cudaStreamSynchronize(c->stream));
+  c->tab_n = 0;
+  c->published = 0;
+  c->stream_bufs.clear();
+  c->last_bad = ~0ull;
+  c->stream_open = true;
+  return NQ_OK;
+}
+
+int ctx_stream_launch(nq_ctx* c, int n, int pre_rows, int variant) {
+  if (!c || !c->stream_open) return set_error(NQ_ECONFIG, "no streaming launch begun");
+  if (int rc = check_args(n, pre_rows, variant)) return rc;
+  NQ_CUDA(cudaSetDevice(c->device));
+  if (int rc = enqueue(c, n, pre_rows, variant, nullptr, 0, false, nullptr, nullptr, nullptr))
+    return rc;
+  c->pending = true;
+  c->p_variant = variant;
+  c->p_h2d = false;
+  c->p_pre_rows = pre_rows;
+  c->p_count = 0;
+  return NQ_OK;
+}
+
+int ctx_stream_stage(nq_ctx* c, const nq_sub* host, uint64_t first, uint64_t len,
+                     const nq_sub** dev_base) {
+  if (first + len > c->d_cap) return set_error(NQ_ECONFIG, "staged chunk beyond the device buffer");
+  NQ_CUDA(cudaMemcpyAsync(c->d_subs + first, host + first, len * sizeof(nq_sub),
+                          cudaMemcpyHostToDevice, c->side));
+  *dev_base = reinterpret_cast<const nq_sub*>(c->d_subs + first);
+  return NQ_OK;
+}
+
+int ctx_stream_expand(nq_ctx* c, int n, int target, const nq_sub* host_roots, uint64_t count,
+                      const nq_sub** dev_base, uint64_t* total) {
+  *dev_base = nullptr;
+  *total = 0;
+  if (count == 0) return NQ_OK;
+  uint4* d_roots = nullptr;
+  NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), count * 16, c->side));
+  NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                          c->side));
+  uint4* deep = nullptr;
+  const int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count, target,
+                               c->side, &deep, total);
+  cudaFreeAsync(d_roots, c->side);
+  if (rc) {
+    if (deep) cudaFreeAsync(deep, c->side);
+    return rc;
+  }
+  if (deep) c->stream_bufs.push_back(deep);
+  *dev_base = reinterpret_cast<const nq_sub*>(deep);
+  return NQ_OK;
+}
+
+int ctx_stream_push(nq_ctx* c, const nq_sub* dev_base, uint64_t len) {
+  if (len == 0) return NQ_OK;
+  if (c->tab_n >= c->tab_cap) return set_error(NQ_ECONFIG, "streaming chunk table is full");
+  c->h_tab[c->tab_n] = QChunk{reinterpret_cast<const uint4*>(dev_base), c->published + len};
+  NQ_CUDA(cudaMemcpyAsync(c->d_tab + c->tab_n, c->h_tab + c->tab_n, sizeof(QChunk),
+                          cudaMemcpyHostToDevice, c->side));
+  c->published += len;
+  c->h_ctl[11] = c->published;
+  // stream order: records (staged / deepened on this stream), then the entry, then the count
+  NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 9, c->h_ctl + 11, sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, c->side));
+  NQ_CUDA(cudaStreamSynchronize(c->side));  // h_ctl[11] is rewritten by the next publish
+  ++c->tab_n;
+  return NQ_OK;
+}
+
+int ctx_stream_consumed(nq_ctx* c, uint64_t* consumed) {
+  NQ_CUDA(cudaMemcpyAsync(c->h_ctl + 12, c->d_ctl, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, c->side));
+  NQ_CUDA(cudaStreamSynchronize(c->side));
+  *consumed = std::min<uint64_t>(c->h_ctl[12], c->published);
+  return NQ_OK;
+}
+
+int ctx_stream_close(nq_ctx* c, bool cancel) {
+  if (cancel) {
+    c->h_ctl[10] = 1;
+    NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 10, sizeof(unsigned long long),
+                            cudaMemcpyHostToDevice, c->side));
+  }
+  c->h_ctl[11] = c->published | kQueueClosed;
+  NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 9, c->h_ctl + 11, sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, c->side));
+  NQ_CUDA(cudaStreamSynchronize(c->side));
+  return NQ_OK;
+}
+
+uint64_t ctx_stream_published(const nq_ctx* c) { return c->published; }
+
+uint64_t ctx_lanes(nq_ctx* c, int n, int pre_rows) {
+  Launch L;
+  if (plan_launch(c, n, pre_rows, false, &L)) return 0;
+  return static_cast<uint64_t>(L.grid) * static_cast<uint64_t>(L.block);
+}
+
 int ctx_mark_start(nq_ctx* c) {
   NQ_CUDA(cudaSetDevice(c->device));
   NQ_CUDA(cudaEventRecord(c->ev_start, c->stream));
@@ -427,7 +562,7 @@ int nq_ctx_create(int device, nq_ctx** out) {
   NQ_CUDA(cudaEventCreate(&c->ev_k1));
   NQ_CUDA(cudaEventCreate(&c->ev_start));
   if (int rc = set_kernel_attributes(device)) return rc;
-  NQ_CUDA(cudaMalloc(&c->d_ctl, 8 * sizeof(unsigned long long)));
+  NQ_CUDA(cudaMalloc(&c->d_ctl, 16 * sizeof(unsigned long long)));
   NQ_CUDA(cudaMallocHost(&c->h_ctl, 16 * sizeof(unsigned long long)));
   *out = c.release();
   return NQ_OK;
@@ -442,6 +577,8 @@ void nq_ctx_destroy(nq_ctx* c) {
   if (c->d_each_nodes) cudaFree(c->d_each_nodes);
   if (c->d_each_high) cudaFree(c->d_each_high);
   if (c->d_ctl) cudaFree(c->d_ctl);
+  if (c->d_tab) cudaFree(c->d_tab);
+  if (c->h_tab) cudaFreeHost(c->h_tab);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
   if (c->ev_k0) cudaEventDestroy(c->ev_k0);
@@ -494,7 +631,13 @@ int nq_collect(nq_ctx* c, nq_result* out) {
   if (!c || !c->pending) return set_error(NQ_ECONFIG, "no batch in flight");
   c->pending = false;
   NQ_CUDA(cudaSetDevice(c->device));
-  return finish(c, c->p_variant, c->p_h2d, c->p_pre_rows, out);
+  const int rc = finish(c, c->p_variant, c->p_h2d, c->p_pre_rows, out);
+  if (c->stream_open) {  // streaming launch done: release the deepened chunks
+    for (void* b : c->stream_bufs) cudaFreeAsync(b, c->stream);
+    c->stream_bufs.clear();
+    c->stream_open = false;
+  }
+  return rc;
 }
 
 int nq_count_device(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,

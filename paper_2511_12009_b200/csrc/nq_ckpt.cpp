@@ -300,6 +300,7 @@ extern "C" int nq_solve_checkpointed(int n, int pre_rows, const nq_solve_opts* o
         st.processed += len;
         st.nodes += r.nodes;
         st.chunks += 1;
+        st.launches += 1;
         st.kernel_ms += r.kernel_ms;
         if (__builtin_add_overflow(st.partial_sum, r.solutions, &st.partial_sum)) {
           rc = set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");

@@ -42,7 +42,8 @@ struct DfsParams {
   const unsigned long long* stop;    // non-zero: hand out no more records (cancel)
   unsigned long long* totals;        // [0] weighted, [1] raw sols, [2] iterations,
                                      // [3] subproblems, [4] first bad record + 1,
-                                     // [6] weighted sum wrapped 64 bits (-> NQ_EOVERFLOW)
+                                     // [6] weighted sum wrapped 64 bits (-> NQ_EOVERFLOW),
+                                     // [7] streaming queue watchdog fired
   unsigned long long* each_count;    // per-record outputs (PER_SUB only)
   int* each_high;
   unsigned long long* each_nodes;
@@ -52,7 +53,25 @@ struct DfsParams {
   int reverse;                       // dispatch order: 1 = last record first
   int lastrow;                       // variant (affects high-water / node outputs only)
   int donate;                        // tail balancing: idle lanes take busy lanes' frames
+  // Streaming launch (stream != 0): records come from a queue of chunks the host
+  // publishes while the kernel runs (nq_sched.cpp's dynamic dispatch), not from
+  // subs[0, count). Chunk j holds the queue positions [q_tab[j-1].end, q_tab[j].end) at
+  // q_tab[j].base; *q_pub = positions published so far, bit 63 = no more will come.
+  int stream;
+  const struct QChunk* q_tab;
+  const unsigned long long* q_pub;
 };
+
+// One published chunk of a streaming launch (written by host copies, read volatile).
+struct QChunk {
+  const uint4* base;
+  unsigned long long end;  // cumulative queue position one past this chunk's last record
+};
+constexpr unsigned long long kQueueClosed = 1ull << 63;
+constexpr unsigned long long kNoTicket = ~0ull;
+// A warp that waits longer than this for the host to publish gives up (the queue is
+// treated as closed and the launch reports it): a host that died cannot hang the GPU.
+constexpr unsigned long long kQueueWatchdogNs = 120ull * 1000000000ull;
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
                                        uint32_t w) {
@@ -233,8 +252,44 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   unsigned long long cur_idx = 0ull, sub_sol = 0ull, sub_it = 0ull;
   int placed = 0, high = 0;
 
-  bool exhausted = false;  // warp-uniform: the dispatch cursor ran past count
+  bool exhausted = false;  // warp-uniform: no more records will be handed to this warp
   uint32_t blocks = 0u;
+  // streaming: this lane's queue position (taken from the cursor, possibly not yet
+  // published by the host) and a monotone hint into the chunk table
+  unsigned long long ticket = kNoTicket;
+  uint32_t chunk = 0u;
+  unsigned long long wait_since = 0ull;
+
+  // Starts record `idx` (reported as the failing index) at `rec` on this lane.
+  // Streaming chunks are copied in while the kernel runs, so their records are read
+  // through L2 (ld.global.cg), never from a possibly stale non-coherent line.
+  auto start = [&](const uint4* rec, unsigned long long idx) {
+    const uint4 s = P.stream ? __ldcg(rec) : __ldg(rec);
+    busy = true;
+    weight = s.w >> 8;
+    placed = static_cast<int>(s.w & 0xffu);
+    if constexpr (PER_SUB) {
+      cur_idx = idx;
+      sub_sol = 0ull;
+      sub_it = 0ull;
+      high = 0;
+    }
+    // Record validation: cols inside the board, one queen per placed row.
+    if ((s.x & ~P.mask) != 0u || __popc(s.x) != placed || placed < P.min_placed) {
+      atomicCAS(P.totals + 4, 0ull, idx + 1ull);
+      weight = 0u;
+    } else if (s.x == P.mask) {
+      sol = 1u;  // fully placed record: cur == last (solver.hpp:89, :148)
+    } else {
+      C = P.mask & ~s.x;
+      l = s.y;
+      r = s.z;
+      a = C & ~(l | r);  // valid_positions (bitboard.hpp:21-23)
+      sp = base1;
+      bp = base1;
+    }
+    if (a == 0u) C = kIdleC;  // settled at the root: back to the idle state
+  };
 
   for (;;) {
     // ---- refill idle lanes (once per KSTEP block) ----------------------------------
@@ -261,51 +316,87 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           busy = false;
         }
         if (exhausted) break;
-        const uint32_t need = __ballot_sync(0xffffffffu, a == 0u);
-        if (need == 0u) break;
-        const uint32_t leader = __ffs(need) - 1u;
-        const uint32_t n_need = __popc(need);
-        unsigned long long first = 0ull;
-        if (lane == leader) {
-          // A raised stop word (host cancel, copied in on a side stream) ends dispatch
-          // at this refill: lanes finish their current subtree, nothing new is taken.
-          first = *reinterpret_cast<const volatile unsigned long long*>(P.stop)
-                      ? P.count
-                      : atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+        if (!P.stream) {
+          const uint32_t need = __ballot_sync(0xffffffffu, a == 0u);
+          if (need == 0u) break;
+          const uint32_t leader = __ffs(need) - 1u;
+          const uint32_t n_need = __popc(need);
+          unsigned long long first = 0ull;
+          if (lane == leader) {
+            // A raised stop word (host cancel, copied in on a side stream) ends dispatch
+            // at this refill: lanes finish their current subtree, nothing new is taken.
+            first = *reinterpret_cast<const volatile unsigned long long*>(P.stop)
+                        ? P.count
+                        : atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+          }
+          first = __shfl_sync(0xffffffffu, first, leader);
+          if (first + n_need >= P.count) exhausted = true;
+          if (a == 0u) {
+            const unsigned long long pos = first + __popc(need & ((1u << lane) - 1u));
+            if (pos < P.count) {
+              const unsigned long long idx = P.reverse ? (P.count - 1ull - pos) : pos;
+              start(&P.subs[idx], idx);
+            }
+          }
+          continue;
         }
-        first = __shfl_sync(0xffffffffu, first, leader);
-        if (first + n_need >= P.count) exhausted = true;
-        if (a == 0u) {
-          const unsigned long long pos = first + __popc(need & ((1u << lane) - 1u));
-          if (pos < P.count) {
-            const unsigned long long idx = P.reverse ? (P.count - 1ull - pos) : pos;
-            const uint4 s = __ldg(&P.subs[idx]);
-            busy = true;
-            weight = s.w >> 8;
-            placed = static_cast<int>(s.w & 0xffu);
-            if constexpr (PER_SUB) {
-              cur_idx = idx;
-              sub_sol = 0ull;
-              sub_it = 0ull;
-              high = 0;
-            }
-            // Record validation: cols inside the board, one queen per placed row.
-            if ((s.x & ~P.mask) != 0u || __popc(s.x) != placed || placed < P.min_placed) {
-              atomicCAS(P.totals + 4, 0ull, idx + 1ull);
-              weight = 0u;
-            } else if (s.x == P.mask) {
-              sol = 1u;  // fully placed record: cur == last (solver.hpp:89, :148)
-            } else {
-              C = P.mask & ~s.x;
-              l = s.y;
-              r = s.z;
-              a = C & ~(l | r);  // valid_positions (bitboard.hpp:21-23)
-              sp = base1;
-              bp = base1;
-            }
-            if (a == 0u) C = kIdleC;  // settled at the root: back to the idle state
+        // Streaming: (1) idle lanes without a queue position take one from the cursor,
+        const uint32_t need = __ballot_sync(0xffffffffu, a == 0u && ticket == kNoTicket);
+        unsigned long long taken_end = 0ull;
+        if (need) {
+          const uint32_t leader = __ffs(need) - 1u;
+          const uint32_t n_need = __popc(need);
+          unsigned long long first = 0ull;
+          if (lane == leader) first = atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+          first = __shfl_sync(0xffffffffu, first, leader);
+          if ((need >> lane) & 1u) ticket = first + __popc(need & ((1u << lane) - 1u));
+          taken_end = first + n_need;
+        }
+        // (2) positions the host has published become records; past the final count
+        // (queue closed, or cancelled) they are dropped,
+        const uint32_t holders = __ballot_sync(0xffffffffu, ticket != kNoTicket);
+        if (holders == 0u) break;
+        const uint32_t reader = __ffs(holders) - 1u;
+        unsigned long long pw = 0ull;
+        if (lane == reader) {
+          pw = *reinterpret_cast<const volatile unsigned long long*>(P.q_pub);
+          if (*reinterpret_cast<const volatile unsigned long long*>(P.stop)) pw = kQueueClosed;
+        }
+        pw = __shfl_sync(0xffffffffu, pw, reader);
+        const unsigned long long pub = pw & ~kQueueClosed;
+        const bool closed = (pw & kQueueClosed) != 0ull;
+        if (ticket != kNoTicket) {
+          if (ticket < pub) {
+            const volatile QChunk* q = reinterpret_cast<const volatile QChunk*>(P.q_tab);
+            unsigned long long end = q[chunk].end;
+            while (ticket >= end) end = q[++chunk].end;
+            const uint4* base = q[chunk].base;
+            // expensive end of the chunk first, like the contiguous launch (reverse)
+            start(base + (end - 1ull - ticket), ticket);
+            ticket = kNoTicket;
+          } else if (closed) {
+            ticket = kNoTicket;
           }
         }
+        if (closed && need && taken_end >= pub) exhausted = true;
+        // (3) positions still unpublished: step the busy lanes and look again after
+        // KSTEP steps; if no lane has work, nap instead of spinning on the cursor.
+        if (__ballot_sync(0xffffffffu, ticket != kNoTicket) == 0u) continue;
+        if (__all_sync(0xffffffffu, a == 0u)) {
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (wait_since == 0ull) wait_since = now;
+          if (now - wait_since > kQueueWatchdogNs) {  // the host stopped publishing
+            atomicExch(P.totals + 7, 1ull);
+            ticket = kNoTicket;
+            exhausted = true;
+            break;
+          }
+          __nanosleep(500);
+          continue;
+        }
+        wait_since = 0ull;
+        break;
       }
       if constexpr (!PER_SUB) {
         // Tail balancing inside the warp. Once the queue is empty, an idle lane takes

@@ -272,17 +272,15 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
       const std::string range_name = "nq_solve_batch worker " + std::to_string(w);
       NvtxRange range(range_name.c_str());
       const auto s0 = clk::now();
-      // Two contexts per worker: dynamic strategies keep one launch running while the
-      // next is enqueued, so a chunk's tail overlaps the next chunk's first blocks.
-      nq_ctx* cx[2] = {nullptr, nullptr};
+      nq_ctx* cx[2] = {nullptr, nullptr};  // [0]: this worker's context
       struct Flight {
         bool busy = false;
         uint64_t first = 0, len = 0, work = 0;
       } fl[2];
       uint64_t bad_first = 0, bad_len = 0;  // the launch that failed (for the message)
+      uint64_t bad_record = ~0ull;           // streaming: the rejected record's batch index
       bool strided_index = false;
-      int rc = pooled_ctx(st.device, 2 * slot[w], &cx[0]);
-      if (rc == NQ_OK && dynamic) rc = pooled_ctx(st.device, 2 * slot[w] + 1, &cx[1]);
+      int rc = pooled_ctx(st.device, slot[w], &cx[0]);
       for (nq_ctx* c : cx)
         if (c) nq_ctx_set_cancel(c, o.cancel);
       if (rc == NQ_OK) rc = ctx_mark_start(cx[0]);
@@ -314,8 +312,90 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         st.processed += r.subproblems;
         st.nodes += r.nodes;
         st.chunks += 1;
+        st.launches += 1;
         st.kernel_ms += r.kernel_ms;
         st.span_ms = std::max(st.span_ms, ctx_span_ms(cx[0], cx[i]));
+        return NQ_OK;
+      };
+      // Dynamic strategies: ONE persistent streaming launch per worker, fed chunk by chunk
+      // from the dispenser while it runs (ctx_stream_*): the GPU never drains between
+      // chunks, and the host keeps only a small lead of published-but-untaken records
+      // (low_water) so that the last chunks still balance across devices.
+      auto stream_worker = [&](int wk, nq_ctx* c, nq_worker_stats& ws) -> int {
+        struct Pushed {
+          uint64_t vstart, first, len, records;
+        };
+        std::vector<Pushed> pushed;
+        uint64_t floor = 1;
+        nq_dispatch_info(disp, nullptr, nullptr, &floor, nullptr);
+        const uint64_t max_chunks = std::min<uint64_t>(count + 1, count / std::max<uint64_t>(floor, 1) + 4096);
+        const uint64_t lanes = ctx_lanes(c, n, launch_rows);
+        const uint64_t low_water = kind == kLaunchExpand ? std::max<uint64_t>(lanes, 4096)
+                                                         : std::max<uint64_t>(lanes / 8, 4096);
+        int e = ctx_stream_begin(c, max_chunks, kind == kLaunchHost ? count : 0);
+        if (e == NQ_OK) e = ctx_stream_launch(c, n, launch_rows, o.variant);
+        if (e) return e;
+        bool cancelled = false;
+        while (e == NQ_OK) {
+          if (cancel_raised(o.cancel)) {
+            cancelled = true;
+            interrupted.store(true);
+            break;
+          }
+          uint64_t consumed = 0;
+          if ((e = ctx_stream_consumed(c, &consumed))) break;
+          const uint64_t pub = ctx_stream_published(c);
+          if (pub - consumed >= low_water) {
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+            continue;
+          }
+          uint64_t f = 0, l = 0;
+          const int got = nq_dispatch_take(disp, &f, &l);
+          if (got < 0) {
+            e = got;
+            break;
+          }
+          if (got == 0) break;  // dispenser drained: close the queue below
+          const nq_sub* base = nullptr;
+          uint64_t recs = l;
+          if (kind == kLaunchHost) e = ctx_stream_stage(c, src, f, l, &base);
+          else if (kind == kLaunchDevice) base = src + f;
+          else e = ctx_stream_expand(c, n, target_rows, src + f, l, &base, &recs);
+          if (e) {
+            bad_first = f;
+            bad_len = l;
+            break;
+          }
+          pushed.push_back(Pushed{pub, f, l, recs});
+          e = ctx_stream_push(c, base, recs);
+        }
+        const int ce = ctx_stream_close(c, cancelled || e != NQ_OK);
+        nq_result r{};
+        const int re = nq_collect(c, &r);  // always drain the launch
+        ws.launches += 1;
+        ws.chunks += pushed.size();
+        if (e) return e;
+        if (ce) return ce;
+        if (re) {  // a rejected record: map its queue position back to the batch
+          const uint64_t v = ctx_last_bad(c);
+          for (const Pushed& p : pushed)
+            if (v != ~0ull && v >= p.vstart && v < p.vstart + p.records) {
+              bad_first = p.first;
+              bad_len = p.len;
+              if (kind != kLaunchExpand) bad_record = p.first + (p.vstart + p.records - 1 - v);
+            }
+          return re;
+        }
+        uint64_t work = 0;
+        for (const Pushed& p : pushed) work += p.records;
+        if (r.subproblems < work) interrupted.store(true);  // cancelled inside the launch
+        if (!add_ok(ws.partial_sum, r.solutions, &ws.partial_sum))
+          return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
+        ws.processed += r.subproblems;
+        ws.nodes += r.nodes;
+        ws.kernel_ms += r.kernel_ms;
+        ws.span_ms = std::max(ws.span_ms, ctx_span_ms(cx[0], c));
+        (void)wk;
         return NQ_OK;
       };
       std::vector<nq_sub> gathered;
@@ -353,31 +433,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           }
         } else {
           emit(o, NQ_LOG_START, w, 0, 0.0);
-          int cur = 0;
-          while (rc == NQ_OK && !interrupted.load()) {
-            if (cancel_raised(o.cancel)) {
-              interrupted.store(true);
-              break;
-            }
-            uint64_t f = 0, l = 0;
-            const int got = nq_dispatch_take(disp, &f, &l);
-            if (got < 0) {
-              rc = got;
-              break;
-            }
-            if (got == 0) break;
-            if (fl[cur].busy) rc = collect(cur);  // the launch issued two chunks ago
-            if (rc == NQ_OK) rc = launch(cur, src, f, l);
-            cur ^= 1;
-          }
-          // Drain: the older launch first.
-          for (int k = 0; k < 2; ++k) {
-            const int i = cur ^ k;
-            if (fl[i].busy) {
-              const int e = collect(i);
-              if (rc == NQ_OK) rc = e;
-            }
-          }
+          rc = stream_worker(w, cx[0], st);
         }
       }
       st.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - s0).count();
@@ -389,9 +445,13 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           uint64_t bad = ~0ull;
           for (nq_ctx* c : cx)
             if (c && ctx_last_bad(c) != ~0ull) bad = ctx_last_bad(c);
-          const uint64_t global_bad = strided_index
-                                          ? static_cast<uint64_t>(w) + bad * static_cast<uint64_t>(W)
-                                          : bad_first + bad;
+          uint64_t global_bad = strided_index
+                                    ? static_cast<uint64_t>(w) + bad * static_cast<uint64_t>(W)
+                                    : bad_first + bad;
+          if (dynamic) {
+            global_bad = bad_record;
+            bad = bad_record;
+          }
           std::string where = bad != ~0ull && kind != kLaunchExpand
                                   ? "subproblem " + std::to_string(global_bad)
                                   : "chunk [" + std::to_string(bad_first) + ", " +

@@ -405,6 +405,7 @@ class WorkerStats:
     kernel_ms: float = 0.0
     chunks: int = 0
     span_ms: float = 0.0  # device time, first enqueued operation -> last kernel end
+    launches: int = 0     # kernel launches (dynamic strategies: one streaming launch)
 
 
 @dataclass
@@ -554,7 +555,7 @@ def _report(n: int, pre_rows: int, opts: ExecuteOptions, rep) -> SolveReport:
         r.workers.append(WorkerStats(worker=w.worker, assigned=w.assigned, processed=w.processed,
                                      partial_sum=w.partial_sum, elapsed_ms=w.elapsed_ms,
                                      device=w.device, nodes=w.nodes, kernel_ms=w.kernel_ms,
-                                     chunks=w.chunks, span_ms=w.span_ms))
+                                     chunks=w.chunks, span_ms=w.span_ms, launches=w.launches))
     return r
 
 
