@@ -137,13 +137,15 @@ struct nq_ctx {
   uint64_t p_count = 0;
   uint64_t last_bad = ~0ull;               // index (within the batch) of a rejected record
   uint64_t last_expanded = 0;              // records produced by the last nq_count_expand
-  // streaming launch (ctx_stream_*): the chunk table the host appends to while it runs
-  QChunk* d_tab = nullptr;
-  QChunk* h_tab = nullptr;                 // pinned staging of the same entries
+  // streaming launch (ctx_stream_*): the chunk table the host appends to while it runs,
+  // in mapped pinned memory (the kernel reads it over the bus and mirrors it in d_tab)
+  QChunk* d_tab = nullptr;                 // device mirror, zeroed before each launch
+  QChunk* h_tab = nullptr;                 // mapped pinned host table
+  unsigned long long* h_mbox = nullptr;    // mapped pinned: [0] publish word, [1] progress
   uint64_t tab_cap = 0, tab_n = 0;
   uint64_t published = 0;
   bool stream_open = false;
-  std::vector<void*> stream_bufs;          // deepened chunks, released after the launch
+  uint4* d_deep = nullptr;                 // ctx_deepen output (stream-ordered allocation)
 };
 
 namespace nqb200 {
@@ -264,7 +266,9 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.donate = c->donate;
   P.stream = c->stream_open ? 1 : 0;
   P.q_tab = c->d_tab;
-  P.q_pub = c->d_ctl + 9;
+  P.q_host_tab = c->h_tab;
+  P.q_pub = c->h_mbox;
+  P.q_progress = c->h_mbox ? c->h_mbox + 1 : nullptr;
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
   if (count > 0 || c->stream_open) {
     L.fn<<<L.grid, L.block, L.smem, c->stream>>>(P);
@@ -392,7 +396,10 @@ int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, 
 }
 
 // ---- streaming launch --------------------------------------------------------------------
-int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks, uint64_t host_records) {
+// Everything the kernel sees while it runs goes through mapped pinned host memory: a
+// stream operation (copy, memset, launch) issued now could be queued behind this
+// persistent kernel on a shared hardware queue and never run.
+int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks) {
   if (!c) return set_error(NQ_ECONFIG, "null context");
   if (c->pending) return set_error(NQ_ECONFIG, "a batch is already in flight on this context");
   NQ_CUDA(cudaSetDevice(c->device));
@@ -403,17 +410,17 @@ int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks, uint64_t host_records) {
     c->h_tab = nullptr;
     c->tab_cap = 0;
     NQ_CUDA(cudaMalloc(&c->d_tab, max_chunks * sizeof(QChunk)));
-    NQ_CUDA(cudaMallocHost(&c->h_tab, max_chunks * sizeof(QChunk)));
+    NQ_CUDA(cudaHostAlloc(&c->h_tab, max_chunks * sizeof(QChunk), cudaHostAllocMapped));
     c->tab_cap = max_chunks;
   }
-  if (host_records)
-    if (int rc = ensure_capacity(c, host_records)) return rc;
-  // The reset must land before the first publish (side stream): wait for it here.
+  if (!c->h_mbox)
+    NQ_CUDA(cudaHostAlloc(&c->h_mbox, 2 * sizeof(unsigned long long), cudaHostAllocMapped));
+  __atomic_store_n(&c->h_mbox[0], 0ull, __ATOMIC_RELEASE);
+  __atomic_store_n(&c->h_mbox[1], 0ull, __ATOMIC_RELEASE);
   NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 10 * sizeof(unsigned long long), c->stream));
-  NQ_CUDA(cudaStreamSynchronize(c->stream));
+  NQ_CUDA(cudaMemsetAsync(c->d_tab, 0, max_chunks * sizeof(QChunk), c->stream));
   c->tab_n = 0;
   c->published = 0;
-  c->stream_bufs.clear();
   c->last_bad = ~0ull;
   c->stream_open = true;
   return NQ_OK;
@@ -433,75 +440,71 @@ int ctx_stream_launch(nq_ctx* c, int n, int pre_rows, int variant) {
   return NQ_OK;
 }
 
-int ctx_stream_stage(nq_ctx* c, const nq_sub* host, uint64_t first, uint64_t len,
-                     const nq_sub** dev_base) {
-  if (first + len > c->d_cap) return set_error(NQ_ECONFIG, "staged chunk beyond the device buffer");
-  NQ_CUDA(cudaMemcpyAsync(c->d_subs + first, host + first, len * sizeof(nq_sub),
-                          cudaMemcpyHostToDevice, c->side));
-  *dev_base = reinterpret_cast<const nq_sub*>(c->d_subs + first);
-  return NQ_OK;
-}
-
-int ctx_stream_expand(nq_ctx* c, int n, int target, const nq_sub* host_roots, uint64_t count,
-                      const nq_sub** dev_base, uint64_t* total) {
-  *dev_base = nullptr;
-  *total = 0;
-  if (count == 0) return NQ_OK;
-  uint4* d_roots = nullptr;
-  NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), count * 16, c->side));
-  NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
-                          c->side));
-  uint4* deep = nullptr;
-  const int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count, target,
-                               c->side, &deep, total);
-  cudaFreeAsync(d_roots, c->side);
-  if (rc) {
-    if (deep) cudaFreeAsync(deep, c->side);
-    return rc;
-  }
-  if (deep) c->stream_bufs.push_back(deep);
-  *dev_base = reinterpret_cast<const nq_sub*>(deep);
-  return NQ_OK;
-}
-
 int ctx_stream_push(nq_ctx* c, const nq_sub* dev_base, uint64_t len) {
   if (len == 0) return NQ_OK;
   if (c->tab_n >= c->tab_cap) return set_error(NQ_ECONFIG, "streaming chunk table is full");
-  c->h_tab[c->tab_n] = QChunk{reinterpret_cast<const uint4*>(dev_base), c->published + len};
-  NQ_CUDA(cudaMemcpyAsync(c->d_tab + c->tab_n, c->h_tab + c->tab_n, sizeof(QChunk),
-                          cudaMemcpyHostToDevice, c->side));
+  QChunk& e = c->h_tab[c->tab_n];
+  e.base = reinterpret_cast<const uint4*>(dev_base);
+  e.end = c->published + len;
   c->published += len;
-  c->h_ctl[11] = c->published;
-  // stream order: records (staged / deepened on this stream), then the entry, then the count
-  NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 9, c->h_ctl + 11, sizeof(unsigned long long),
-                          cudaMemcpyHostToDevice, c->side));
-  NQ_CUDA(cudaStreamSynchronize(c->side));  // h_ctl[11] is rewritten by the next publish
   ++c->tab_n;
+  // the entry before the count that makes it visible (the kernel reads with acquire)
+  __atomic_store_n(&c->h_mbox[0], c->published, __ATOMIC_RELEASE);
   return NQ_OK;
 }
 
 int ctx_stream_consumed(nq_ctx* c, uint64_t* consumed) {
-  NQ_CUDA(cudaMemcpyAsync(c->h_ctl + 12, c->d_ctl, sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, c->side));
-  NQ_CUDA(cudaStreamSynchronize(c->side));
-  *consumed = std::min<uint64_t>(c->h_ctl[12], c->published);
+  const uint64_t taken = __atomic_load_n(&c->h_mbox[1], __ATOMIC_ACQUIRE);
+  *consumed = std::min<uint64_t>(taken, c->published);
   return NQ_OK;
 }
 
-int ctx_stream_close(nq_ctx* c, bool cancel) {
-  if (cancel) {
-    c->h_ctl[10] = 1;
-    NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 6, c->h_ctl + 10, sizeof(unsigned long long),
-                            cudaMemcpyHostToDevice, c->side));
-  }
-  c->h_ctl[11] = c->published | kQueueClosed;
-  NQ_CUDA(cudaMemcpyAsync(c->d_ctl + 9, c->h_ctl + 11, sizeof(unsigned long long),
-                          cudaMemcpyHostToDevice, c->side));
-  NQ_CUDA(cudaStreamSynchronize(c->side));
+int ctx_stream_close(nq_ctx* c, bool /*cancel*/) {
+  // A cancel simply stops publishing: what was published and not yet taken (at most
+  // the feeder's lead) is still counted, then the launch ends.
+  __atomic_store_n(&c->h_mbox[0], c->published | kQueueClosed, __ATOMIC_RELEASE);
   return NQ_OK;
 }
 
 uint64_t ctx_stream_published(const nq_ctx* c) { return c->published; }
+
+int ctx_upload(nq_ctx* c, const nq_sub* host, uint64_t count, const nq_sub** dev) {
+  NQ_CUDA(cudaSetDevice(c->device));
+  if (int rc = ensure_capacity(c, count)) return rc;
+  NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
+  if (count)
+    NQ_CUDA(cudaMemcpyAsync(c->d_subs, host, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                            c->stream));
+  *dev = reinterpret_cast<const nq_sub*>(c->d_subs);
+  return NQ_OK;
+}
+
+void ctx_release_deep(nq_ctx* c) {
+  if (c->d_deep) {
+    cudaSetDevice(c->device);
+    cudaFreeAsync(c->d_deep, c->stream);
+  }
+  c->d_deep = nullptr;
+}
+
+int ctx_deepen(nq_ctx* c, int n, int target, const nq_sub* host_roots, uint64_t count,
+               const nq_sub** dev, uint64_t* total) {
+  ctx_release_deep(c);
+  *dev = nullptr;
+  *total = 0;
+  NQ_CUDA(cudaSetDevice(c->device));
+  if (count == 0) return NQ_OK;
+  uint4* d_roots = nullptr;
+  NQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_roots), count * 16, c->stream));
+  NQ_CUDA(cudaMemcpyAsync(d_roots, host_roots, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                          c->stream));
+  const int rc = expand_levels(c->device, n, reinterpret_cast<const nq_sub*>(d_roots), count,
+                               target, c->stream, &c->d_deep, total);
+  cudaFreeAsync(d_roots, c->stream);
+  if (rc) return rc;
+  *dev = reinterpret_cast<const nq_sub*>(c->d_deep);
+  return NQ_OK;
+}
 
 uint64_t ctx_lanes(nq_ctx* c, int n, int pre_rows) {
   Launch L;
@@ -579,6 +582,7 @@ void nq_ctx_destroy(nq_ctx* c) {
   if (c->d_ctl) cudaFree(c->d_ctl);
   if (c->d_tab) cudaFree(c->d_tab);
   if (c->h_tab) cudaFreeHost(c->h_tab);
+  if (c->h_mbox) cudaFreeHost(c->h_mbox);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
   if (c->ev_k0) cudaEventDestroy(c->ev_k0);
@@ -632,11 +636,7 @@ int nq_collect(nq_ctx* c, nq_result* out) {
   c->pending = false;
   NQ_CUDA(cudaSetDevice(c->device));
   const int rc = finish(c, c->p_variant, c->p_h2d, c->p_pre_rows, out);
-  if (c->stream_open) {  // streaming launch done: release the deepened chunks
-    for (void* b : c->stream_bufs) cudaFreeAsync(b, c->stream);
-    c->stream_bufs.clear();
-    c->stream_open = false;
-  }
+  c->stream_open = false;
   return rc;
 }
 

@@ -76,22 +76,25 @@ int ctx_mark_start(nq_ctx* c);
 double ctx_span_ms(const nq_ctx* start, const nq_ctx* end);
 int ctx_device(const nq_ctx* c);
 
-// Streaming launch: ONE persistent counting kernel fed while it runs. begin (reset, size
-// the chunk table, and the host-record buffer when chunks are staged from host memory)
-// -> launch -> any number of push (a device-resident chunk: records of the caller's
-// device copy, staged from host memory, or host roots deepened on the device) -> close
-// -> nq_collect. The kernel hands out published records lane by lane and naps while
-// the queue is empty, so chunks of any size cost no launch and no end-of-launch tail.
-int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks, uint64_t host_records);
+// Streaming launch: ONE persistent counting kernel fed while it runs. begin (reset,
+// size the chunk table) -> launch -> any number of push (a chunk of device-resident
+// records) -> close -> nq_collect. The kernel hands out published records lane by lane
+// and naps while the queue is empty, so chunks of any size cost no launch and no
+// end-of-launch tail. Between launch and collect the host makes NO stream call on the
+// context: table, publish word and progress live in mapped pinned host memory.
+int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks);
 int ctx_stream_launch(nq_ctx* c, int n, int pre_rows, int variant);
-int ctx_stream_stage(nq_ctx* c, const nq_sub* host, uint64_t first, uint64_t len,
-                     const nq_sub** dev_base);
-int ctx_stream_expand(nq_ctx* c, int n, int target, const nq_sub* host_roots, uint64_t count,
-                      const nq_sub** dev_base, uint64_t* total);
 int ctx_stream_push(nq_ctx* c, const nq_sub* dev_base, uint64_t len);
-int ctx_stream_consumed(nq_ctx* c, uint64_t* consumed);  // queue positions taken so far
+int ctx_stream_consumed(nq_ctx* c, uint64_t* consumed);  // queue positions taken (coarse)
 int ctx_stream_close(nq_ctx* c, bool cancel);
 uint64_t ctx_stream_published(const nq_ctx* c);
+// Device-resident copy of a host batch on the context (ensure + H2D on its stream).
+int ctx_upload(nq_ctx* c, const nq_sub* host, uint64_t count, const nq_sub** dev);
+// Host roots deepened on the context's device to `target` rows (stream-ordered, the
+// buffer lives until ctx_release_deep); *total records at *dev.
+int ctx_deepen(nq_ctx* c, int n, int target, const nq_sub* host_roots, uint64_t count,
+               const nq_sub** dev, uint64_t* total);
+void ctx_release_deep(nq_ctx* c);
 uint64_t ctx_lanes(nq_ctx* c, int n, int pre_rows);  // resident lanes of a launch
 
 // execute_batch over records that are deepened to `target_rows` on the device first

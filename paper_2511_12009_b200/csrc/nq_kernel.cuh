@@ -55,15 +55,21 @@ struct DfsParams {
   int donate;                        // tail balancing: idle lanes take busy lanes' frames
   // Streaming launch (stream != 0): records come from a queue of chunks the host
   // publishes while the kernel runs (nq_sched.cpp's dynamic dispatch), not from
-  // subs[0, count). Chunk j holds the queue positions [q_tab[j-1].end, q_tab[j].end) at
-  // q_tab[j].base; *q_pub = positions published so far, bit 63 = no more will come.
+  // subs[0, count). Chunk j holds the queue positions [tab[j-1].end, tab[j].end) at
+  // tab[j].base. The host writes the table and the publish word (positions published,
+  // bit 63 = closed) into MAPPED PINNED HOST memory, never through a stream (a copy
+  // queued behind this persistent kernel would never run); the kernel keeps a device
+  // mirror of the entries it has read and reports its cursor back the same way.
   int stream;
-  const struct QChunk* q_tab;
-  const unsigned long long* q_pub;
+  struct QChunk* q_tab;                        // device mirror (zeroed before launch)
+  const struct QChunk* q_host_tab;             // mapped host table
+  const unsigned long long* q_pub;             // mapped host publish word
+  unsigned long long* q_progress;              // mapped host: cursor, coarsely
 };
 
-// One published chunk of a streaming launch (written by host copies, read volatile).
-struct QChunk {
+// One published chunk of a streaming launch (16-byte aligned: the device mirror is
+// read and written as one 16-byte access, so a reader never sees half an entry).
+struct alignas(16) QChunk {
   const uint4* base;
   unsigned long long end;  // cumulative queue position one past this chunk's last record
 };
@@ -259,6 +265,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   unsigned long long ticket = kNoTicket;
   uint32_t chunk = 0u;
   unsigned long long wait_since = 0ull;
+  unsigned long long pub_seen = 0ull;  // warp-uniform: published positions last read
+  bool closed_seen = false;
 
   // Starts record `idx` (reported as the failing index) at `rec` on this lane.
   // Streaming chunks are copied in while the kernel runs, so their records are read
@@ -347,40 +355,59 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           const uint32_t leader = __ffs(need) - 1u;
           const uint32_t n_need = __popc(need);
           unsigned long long first = 0ull;
-          if (lane == leader) first = atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+          if (lane == leader) {
+            first = atomicAdd(P.cursor, static_cast<unsigned long long>(n_need));
+            // coarse progress for the host's feeder (every 4096 positions)
+            if ((first >> 12) != ((first + n_need) >> 12))
+              asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(P.q_progress),
+                           "l"(first + n_need)
+                           : "memory");
+          }
           first = __shfl_sync(0xffffffffu, first, leader);
           if ((need >> lane) & 1u) ticket = first + __popc(need & ((1u << lane) - 1u));
           taken_end = first + n_need;
         }
         // (2) positions the host has published become records; past the final count
-        // (queue closed, or cancelled) they are dropped,
+        // (queue closed) they are dropped. The publish word is re-read (over the bus)
+        // only when a ticket is beyond what this warp last saw.
         const uint32_t holders = __ballot_sync(0xffffffffu, ticket != kNoTicket);
         if (holders == 0u) break;
-        const uint32_t reader = __ffs(holders) - 1u;
-        unsigned long long pw = 0ull;
-        if (lane == reader) {
-          pw = *reinterpret_cast<const volatile unsigned long long*>(P.q_pub);
-          if (*reinterpret_cast<const volatile unsigned long long*>(P.stop)) pw = kQueueClosed;
+        if (__any_sync(0xffffffffu, ticket != kNoTicket && ticket >= pub_seen) && !closed_seen) {
+          unsigned long long pw = 0ull;
+          if (lane == __ffs(holders) - 1u)
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(pw) : "l"(P.q_pub) : "memory");
+          pw = __shfl_sync(0xffffffffu, pw, __ffs(holders) - 1u);
+          pub_seen = pw & ~kQueueClosed;
+          closed_seen = (pw & kQueueClosed) != 0ull;
         }
-        pw = __shfl_sync(0xffffffffu, pw, reader);
-        const unsigned long long pub = pw & ~kQueueClosed;
-        const bool closed = (pw & kQueueClosed) != 0ull;
         if (ticket != kNoTicket) {
-          if (ticket < pub) {
-            const volatile QChunk* q = reinterpret_cast<const volatile QChunk*>(P.q_tab);
-            unsigned long long end = q[chunk].end;
-            while (ticket >= end) end = q[++chunk].end;
-            const uint4* base = q[chunk].base;
+          if (ticket < pub_seen) {
+            // chunk lookup: the device mirror, filled from the host table on a miss
+            unsigned long long eb, ee;
+            for (;;) {
+              asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(eb), "=l"(ee)
+                           : "l"(P.q_tab + chunk) : "memory");
+              if (ee == 0ull) {  // first reader of this entry: fetch it from the host table
+                asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(eb)
+                             : "l"(&P.q_host_tab[chunk].base) : "memory");
+                asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(ee)
+                             : "l"(&P.q_host_tab[chunk].end) : "memory");
+                asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + chunk), "l"(eb),
+                             "l"(ee) : "memory");
+              }
+              if (ticket < ee) break;
+              ++chunk;
+            }
             // expensive end of the chunk first, like the contiguous launch (reverse)
-            start(base + (end - 1ull - ticket), ticket);
+            start(reinterpret_cast<const uint4*>(eb) + (ee - 1ull - ticket), ticket);
             ticket = kNoTicket;
-          } else if (closed) {
+          } else if (closed_seen) {
             ticket = kNoTicket;
           }
         }
-        if (closed && need && taken_end >= pub) exhausted = true;
+        if (closed_seen && need && taken_end >= pub_seen) exhausted = true;
         // (3) positions still unpublished: step the busy lanes and look again after
-        // KSTEP steps; if no lane has work, nap instead of spinning on the cursor.
+        // KSTEP steps; if no lane has work, nap instead of spinning on the bus.
         if (__ballot_sync(0xffffffffu, ticket != kNoTicket) == 0u) continue;
         if (__all_sync(0xffffffffu, a == 0u)) {
           unsigned long long now;
@@ -392,7 +419,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
             exhausted = true;
             break;
           }
-          __nanosleep(500);
+          __nanosleep(1000);
           continue;
         }
         wait_since = 0ull;

@@ -241,13 +241,22 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
     if (rc) return rc;
   }
   const bool dynamic = o.strategy == NQ_PARTITION_STEALING || o.strategy == NQ_PARTITION_GUIDED;
+  // Dynamic dispatch over roots deepened on the devices hands out ranges of the DEEPENED
+  // stream (every worker deepens all roots; its records are in stream order).
+  uint64_t disp_count = count;
+  if (dynamic && target_rows) {
+    if (o.dispatch)
+      return set_error(NQ_ECONFIG, "a shared dispenser cannot drive device-side deepening");
+    if (int rc = expand(n, subs, count, target_rows, nullptr, 0, &disp_count)) return rc;
+  }
   nq_dispatch* disp = o.dispatch;
   struct DispGuard {
     nq_dispatch* d = nullptr;
     ~DispGuard() { nq_dispatch_close(d, 0); }
   } own_disp;
   if (dynamic && !disp) {
-    if (int rc = nq_dispatch_create(nullptr, count, o.strategy, o.chunk, W, &own_disp.d)) return rc;
+    if (int rc = nq_dispatch_create(nullptr, disp_count, o.strategy, o.chunk, W, &own_disp.d))
+      return rc;
     disp = own_disp.d;
   }
 
@@ -323,18 +332,32 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
       // (low_water) so that the last chunks still balance across devices.
       auto stream_worker = [&](int wk, nq_ctx* c, nq_worker_stats& ws) -> int {
         struct Pushed {
-          uint64_t vstart, first, len, records;
+          uint64_t vstart, first, len;
         };
         std::vector<Pushed> pushed;
+        // The whole batch is made device-resident first (the caller's device copy, one
+        // H2D of host records, or all roots deepened on this device): the running
+        // kernel is then fed by publishing ranges of it, with no stream operation.
+        const nq_sub* all = src;
+        uint64_t all_n = count;
+        int e = NQ_OK;
+        if (kind == kLaunchHost) e = ctx_upload(c, src, count, &all);
+        else if (kind == kLaunchExpand) e = ctx_deepen(c, n, target_rows, src, count, &all, &all_n);
+        if (e == NQ_OK && all_n != disp_count)
+          e = set_error(NQ_ECONFIG, "deepened batch has " + std::to_string(all_n) +
+                                        " records, the dispenser " + std::to_string(disp_count));
         uint64_t floor = 1;
         nq_dispatch_info(disp, nullptr, nullptr, &floor, nullptr);
-        const uint64_t max_chunks = std::min<uint64_t>(count + 1, count / std::max<uint64_t>(floor, 1) + 4096);
+        const uint64_t max_chunks =
+            std::min<uint64_t>(disp_count + 1, disp_count / std::max<uint64_t>(floor, 1) + 4096);
         const uint64_t lanes = ctx_lanes(c, n, launch_rows);
-        const uint64_t low_water = kind == kLaunchExpand ? std::max<uint64_t>(lanes, 4096)
-                                                         : std::max<uint64_t>(lanes / 8, 4096);
-        int e = ctx_stream_begin(c, max_chunks, kind == kLaunchHost ? count : 0);
+        const uint64_t low_water = std::max<uint64_t>(lanes / 8, 4096);
+        if (e == NQ_OK) e = ctx_stream_begin(c, max_chunks);
         if (e == NQ_OK) e = ctx_stream_launch(c, n, launch_rows, o.variant);
-        if (e) return e;
+        if (e) {
+          if (kind == kLaunchExpand) ctx_release_deep(c);
+          return e;
+        }
         bool cancelled = false;
         while (e == NQ_OK) {
           if (cancel_raised(o.cancel)) {
@@ -343,10 +366,10 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
             break;
           }
           uint64_t consumed = 0;
-          if ((e = ctx_stream_consumed(c, &consumed))) break;
+          ctx_stream_consumed(c, &consumed);
           const uint64_t pub = ctx_stream_published(c);
           if (pub - consumed >= low_water) {
-            std::this_thread::sleep_for(std::chrono::microseconds(50));
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
             continue;
           }
           uint64_t f = 0, l = 0;
@@ -356,39 +379,29 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
             break;
           }
           if (got == 0) break;  // dispenser drained: close the queue below
-          const nq_sub* base = nullptr;
-          uint64_t recs = l;
-          if (kind == kLaunchHost) e = ctx_stream_stage(c, src, f, l, &base);
-          else if (kind == kLaunchDevice) base = src + f;
-          else e = ctx_stream_expand(c, n, target_rows, src + f, l, &base, &recs);
-          if (e) {
-            bad_first = f;
-            bad_len = l;
-            break;
-          }
-          pushed.push_back(Pushed{pub, f, l, recs});
-          e = ctx_stream_push(c, base, recs);
+          pushed.push_back(Pushed{pub, f, l});
+          e = ctx_stream_push(c, all + f, l);
         }
-        const int ce = ctx_stream_close(c, cancelled || e != NQ_OK);
+        ctx_stream_close(c, cancelled || e != NQ_OK);
         nq_result r{};
         const int re = nq_collect(c, &r);  // always drain the launch
+        if (kind == kLaunchExpand) ctx_release_deep(c);
         ws.launches += 1;
         ws.chunks += pushed.size();
         if (e) return e;
-        if (ce) return ce;
         if (re) {  // a rejected record: map its queue position back to the batch
           const uint64_t v = ctx_last_bad(c);
           for (const Pushed& p : pushed)
-            if (v != ~0ull && v >= p.vstart && v < p.vstart + p.records) {
+            if (v != ~0ull && v >= p.vstart && v < p.vstart + p.len) {
               bad_first = p.first;
               bad_len = p.len;
-              if (kind != kLaunchExpand) bad_record = p.first + (p.vstart + p.records - 1 - v);
+              if (kind != kLaunchExpand) bad_record = p.first + (p.vstart + p.len - 1 - v);
             }
           return re;
         }
         uint64_t work = 0;
-        for (const Pushed& p : pushed) work += p.records;
-        if (r.subproblems < work) interrupted.store(true);  // cancelled inside the launch
+        for (const Pushed& p : pushed) work += p.len;
+        if (r.subproblems < work || cancelled) interrupted.store(true);
         if (!add_ok(ws.partial_sum, r.solutions, &ws.partial_sum))
           return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
         ws.processed += r.subproblems;
