@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -120,7 +121,7 @@ struct nq_ctx {
   int* d_each_high = nullptr;
   size_t each_cap = 0;
   // [0] cursor, [1..5] totals, [6] stop word, [7] weighted-sum overflow flag,
-  // [8] streaming watchdog flag, [9] streaming publish word (count | closed << 63)
+  // [8] streaming watchdog flag, [9] device mirror of the streaming publish word
   unsigned long long* d_ctl = nullptr;
   // pinned: [0..9] mirror of d_ctl, [10] stop source, [11] publish staging, [12] cursor read
   unsigned long long* h_ctl = nullptr;
@@ -269,6 +270,7 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.q_host_tab = c->h_tab;
   P.q_pub = c->h_mbox;
   P.q_progress = c->h_mbox ? c->h_mbox + 1 : nullptr;
+  P.q_pub_mirror = c->d_ctl + 9;
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
   if (count > 0 || c->stream_open) {
     L.fn<<<L.grid, L.block, L.smem, c->stream>>>(P);
@@ -558,6 +560,10 @@ int nq_ctx_create(int device, nq_ctx** out) {
     return set_error(NQ_ECUDA, std::string("device ") + prop.name +
                                    " is not sm_100-class; this build targets sm_100a only");
   c->sms = prop.multiProcessorCount;
+  // NQB_BLOCKS_PER_SM caps the resident blocks per SM of every new context (default: the
+  // occupancy limit). tools/scaling_emulation.py uses it to run k workers on ONE B200,
+  // each with 1/k of every SM, as an emulation of k GPUs.
+  if (const char* e = std::getenv("NQB_BLOCKS_PER_SM")) c->blocks_per_sm = std::max(0, std::atoi(e));
   NQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   NQ_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   NQ_CUDA(cudaEventCreate(&c->ev_h2d));

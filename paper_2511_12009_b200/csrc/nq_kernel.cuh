@@ -65,6 +65,7 @@ struct DfsParams {
   const struct QChunk* q_host_tab;             // mapped host table
   const unsigned long long* q_pub;             // mapped host publish word
   unsigned long long* q_progress;              // mapped host: cursor, coarsely
+  unsigned long long* q_pub_mirror;            // device: newest publish word any warp read
 };
 
 // One published chunk of a streaming launch (16-byte aligned: the device mirror is
@@ -267,6 +268,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   unsigned long long wait_since = 0ull;
   unsigned long long pub_seen = 0ull;  // warp-uniform: published positions last read
   bool closed_seen = false;
+  const uint4* chunk_base = nullptr;   // this lane's cached chunk entry (end 0: none)
+  unsigned long long chunk_end = 0ull;
 
   // Starts record `idx` (reported as the failing index) at `rec` on this lane.
   // Streaming chunks are copied in while the kernel runs, so their records are read
@@ -373,9 +376,20 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         const uint32_t holders = __ballot_sync(0xffffffffu, ticket != kNoTicket);
         if (holders == 0u) break;
         if (__any_sync(0xffffffffu, ticket != kNoTicket && ticket >= pub_seen) && !closed_seen) {
+          // the device mirror first (one warp per publish pays the bus read)
           unsigned long long pw = 0ull;
-          if (lane == __ffs(holders) - 1u)
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(pw) : "l"(P.q_pub) : "memory");
+          if (lane == __ffs(holders) - 1u) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(pw) : "l"(P.q_pub_mirror) : "memory");
+            if ((pw & ~kQueueClosed) <= pub_seen && !(pw & kQueueClosed)) {
+              unsigned long long ph;
+              asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(ph) : "l"(P.q_pub) : "memory");
+              if (ph > pw) {
+                asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(P.q_pub_mirror), "l"(ph)
+                             : "memory");
+                pw = ph;
+              }
+            }
+          }
           pw = __shfl_sync(0xffffffffu, pw, __ffs(holders) - 1u);
           pub_seen = pw & ~kQueueClosed;
           closed_seen = (pw & kQueueClosed) != 0ull;
@@ -383,8 +397,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         if (ticket != kNoTicket) {
           if (ticket < pub_seen) {
             // chunk lookup: the device mirror, filled from the host table on a miss
-            unsigned long long eb, ee;
-            for (;;) {
+            unsigned long long eb = reinterpret_cast<unsigned long long>(chunk_base), ee = chunk_end;
+            while (ticket >= ee) {  // tickets only grow: move to the entry holding this one
+              if (ee != 0ull) ++chunk;
               asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(eb), "=l"(ee)
                            : "l"(P.q_tab + chunk) : "memory");
               if (ee == 0ull) {  // first reader of this entry: fetch it from the host table
@@ -395,9 +410,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
                 asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + chunk), "l"(eb),
                              "l"(ee) : "memory");
               }
-              if (ticket < ee) break;
-              ++chunk;
             }
+            chunk_base = reinterpret_cast<const uint4*>(eb);
+            chunk_end = ee;
             // expensive end of the chunk first, like the contiguous launch (reverse)
             start(reinterpret_cast<const uint4*>(eb) + (ee - 1ull - ticket), ticket);
             ticket = kNoTicket;

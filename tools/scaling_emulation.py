@@ -1,53 +1,52 @@
 #!/usr/bin/env python3
-"""k-GPU makespan of the product's GUIDED dispatcher, emulated on one B200.
+"""k-GPU runs of the product's dynamic dispatcher, emulated on ONE B200.
 
-The multi-GPU path (nq_sched.cpp) has no inter-GPU traffic: host threads (or one process
-per GPU, torchrun) take guided chunks from ONE dispenser (nq_dispatch_*), each GPU counts
-the chunks it takes, partials are summed on the host. A k-GPU run's time is therefore
-set by the chunk sequence the dispenser hands out for W = k and by each chunk's time on
-one GPU. This tool
+The multi-GPU path (nq_sched.cpp) has no inter-GPU traffic: each GPU runs one persistent
+streaming launch that its host thread feeds with chunks from ONE guided dispenser
+(nq_dispatch_*), and the per-GPU partials are summed on the host. This tool runs exactly
+that code with k workers on device 0 (devices = [0] * k), each worker's launch capped at
+8/k resident blocks per SM (NQB_BLOCKS_PER_SM) so that every worker owns 1/k of every SM:
+k "virtual GPUs" of 1/k of a B200 each, fed by the real dispenser and feeders.
 
-  1. drains a dispenser created exactly as the scheduler creates it (count, guided,
-     floor count/(128 k), W = k) to get the chunk sequence;
-  2. times every chunk ALONE on the one GPU available (CUDA events; device-resident
-     R-records for --mode records = bench.py's `value` path, or the chunk's coarse roots
-     deepened on the device for --mode roots = execute()'s path);
-  3. list-schedules the chunks onto k GPUs in dispenser order (each GPU takes the next
-     chunk when its current one ends) and reports the makespan T_k and the strong-scaling
-     efficiency T_1 / (k T_k).
+On one device the total hardware is fixed, so perfect balance gives T_k = T_1 and the
+efficiency is T_1 / T_k, with T_k = the slowest worker's device span (CUDA events: first
+operation -> end of its kernel). Caveat: when a virtual GPU runs dry its blocks leave
+the SMs and the remaining workers' blocks get a larger share of each SM, which a real
+idle GPU would not give them; the emulated end-phase imbalance is therefore a lower bound.
 
-Each chunk is timed with its own end-of-launch tail, which the scheduler's two launches
-in flight per GPU hide, so T_k is conservative.
-
-    python tools/scaling_emulation.py --n 20 --pre-rows 7 --ks 1,2,4,8 --mode records
+    python tools/scaling_emulation.py --n 20 --pre-rows 7 --ks 1,2,4,8
 """
 from __future__ import annotations
 
 import argparse
-import ctypes
-import heapq
 import json
 import os
+import subprocess
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
 
 
-def chunks_for(nq, count, k):
-    with nq.Dispatcher.create(count, nq.PartitionStrategy.guided, 0, k) as d:
-        out = []
-        while (c := d.take()) is not None:
-            out.append(c)
-        return out
-
-
-def makespan(times, k):
-    """Greedy list scheduling in dispenser order onto k GPUs."""
-    free = [0.0] * k
-    heapq.heapify(free)
-    for t in times:
-        heapq.heappush(free, heapq.heappop(free) + t)
-    return max(free)
+def one(n, r, k, reps, mode):
+    import numpy as np
+    import torch
+    from paper_2511_12009_b200 import nqueens as nq
+    recs = nq.generate_packed(n, r)
+    opts = nq.ExecuteOptions(config=nq.builtin_configs[0],
+                             plan=nq.PartitionPlan(nq.PartitionStrategy.guided, k, [], 0),
+                             devices=[0] * k)
+    dev = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).cuda()
+    best = None
+    for _ in range(reps):
+        rep = nq.execute_batch_device(n, r, [dev.data_ptr()] * k, len(recs), opts)
+        span = max(w.span_ms for w in rep.workers)
+        if best is None or span < best[0]:
+            best = (span, rep)
+    span, rep = best
+    return {"k": k, "T_k_ms": span, "spans_ms": [round(w.span_ms, 2) for w in rep.workers],
+            "chunks": [w.chunks for w in rep.workers], "solutions": rep.total, "nodes": rep.nodes,
+            "blocks_per_sm": int(os.environ.get("NQB_BLOCKS_PER_SM", "0"))}
 
 
 def main():
@@ -55,62 +54,27 @@ def main():
     ap.add_argument("--n", type=int, default=20)
     ap.add_argument("--pre-rows", type=int, default=7)
     ap.add_argument("--ks", default="1,2,4,8")
-    ap.add_argument("--mode", default="records", choices=["records", "roots"])
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--blocks", type=int, default=8, help="resident blocks per SM of one GPU")
+    ap.add_argument("--child", type=int, default=0)
     args = ap.parse_args()
-
-    import numpy as np
-    import torch
-    from paper_2511_12009_b200 import _lib
-    from paper_2511_12009_b200 import nqueens as nq
-
-    ctx = ctypes.c_void_p()
-    _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(ctx)))
-    if args.mode == "records":
-        recs = nq.generate_packed(args.n, args.pre_rows)
-        dev = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).cuda()
-        base = dev.data_ptr()
-    else:
-        coarse = max(2, args.pre_rows - 3)
-        recs = nq.generate_packed(args.n, coarse)
-
-    def time_chunk(f, n):
-        r = _lib.NqResult()
-        if args.mode == "records":
-            _lib.check(_lib.lib.nq_count_device(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
-                                                ctypes.c_void_p(base + 16 * f), n, ctypes.byref(r)))
-            return r.kernel_ms, r.solutions, r.nodes
-        part = np.ascontiguousarray(recs[f:f + n])
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        _lib.check(_lib.lib.nq_count_expand(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
-                                            part.ctypes.data, n, ctypes.byref(r)))
-        ev1.record()
-        torch.cuda.synchronize()
-        # the expand call runs on the context's own stream; bracket it on the host side
-        return max(ev0.elapsed_time(ev1), r.kernel_ms), r.solutions, r.nodes
-
-    time_chunk(0, min(len(recs), 4096))  # warm
+    if args.child:
+        print(json.dumps(one(args.n, args.pre_rows, args.child, args.reps, "device")))
+        return
     t1 = None
     for k in [int(x) for x in args.ks.split(",")]:
-        seq = chunks_for(nq, len(recs), k)
-        times, sols, nodes = [], 0, 0
-        for f, n in seq:
-            ms, s, nd = time_chunk(f, n)
-            times.append(ms)
-            sols += s
-            nodes += nd
-        tk = makespan(times, k)
+        # enough hardware queues for k concurrent persistent launches on one device
+        env = {**os.environ, "NQB_BLOCKS_PER_SM": str(max(1, args.blocks // k)),
+               "CUDA_DEVICE_MAX_CONNECTIONS": "32"}
+        out = subprocess.run([sys.executable, __file__, "--n", str(args.n), "--pre-rows",
+                              str(args.pre_rows), "--reps", str(args.reps), "--child", str(k)],
+                             capture_output=True, text=True, env=env, check=True).stdout
+        row = json.loads(out.strip().splitlines()[-1])
         if k == 1:
-            t1 = tk
-        row = {"mode": args.mode, "n": args.n, "pre_rows": args.pre_rows, "k": k,
-               "chunks": len(seq), "sum_chunk_ms": round(sum(times), 3), "T_k_ms": round(tk, 3),
-               "ideal_ms": round(sum(times) / k, 3), "solutions": sols, "nodes": nodes,
-               "nodes_per_s_k_gpus": nodes / (tk * 1e-3),
-               "efficiency": (t1 / (k * tk)) if t1 else None,
-               "largest_chunk_ms": round(max(times), 3), "last_chunks_ms": [round(t, 3) for t in times[-4:]]}
+            t1 = row["T_k_ms"]
+        row["efficiency"] = t1 / row["T_k_ms"] if t1 else None
+        row["virtual_gpu"] = f"1/{k} of every SM ({max(1, args.blocks // k)} blocks/SM)"
         print(json.dumps(row), flush=True)
-    _lib.lib.nq_ctx_destroy(ctx)
 
 
 if __name__ == "__main__":
