@@ -164,8 +164,9 @@ int nq_partition_weighted(uint64_t task_count, const double* weights, int worker
 #define NQ_PARTITION_UNIFORM 0  /* PartitionStrategy::uniform  (scheduler.hpp:26)        */
 #define NQ_PARTITION_WEIGHTED 1 /* PartitionStrategy::weighted                          */
 #define NQ_PARTITION_STEALING 2 /* PartitionStrategy::stealing: fixed chunks, cursor    */
-#define NQ_PARTITION_GUIDED 3   /* shrinking chunks, expensive end first                */
-#define NQ_PARTITION_STRIDED 4  /* GPU default: record i -> worker i mod W, one launch   */
+#define NQ_PARTITION_GUIDED 3   /* shrinking chunks, expensive end first; the default    */
+                                /* when opts == NULL (one streaming launch per device)   */
+#define NQ_PARTITION_STRIDED 4  /* record i -> worker i mod W, one launch per worker     */
 
 #define NQ_LOG_GENERATION 0 /* "Use %.2fms to generate %llu subproblems!"               */
 #define NQ_LOG_START 1      /* "worker [%d] start job, with %llu(%.2f) subproblems."     */

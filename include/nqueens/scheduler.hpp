@@ -452,8 +452,9 @@ inline SolveReport execute(int n, int pre_rows, const ExecuteOptions& opts) {
         if (opts.log) opts.log(log_result_line(1, 1, 0.0));
         return report;
     }
-    if (opts.plan.strategy == PartitionStrategy::strided) {
-        // nq_solve generates the frontier itself and, from 2^20 records up, deals a
+    if (opts.plan.strategy == PartitionStrategy::strided ||
+        opts.plan.strategy == PartitionStrategy::guided) {
+        // nq_solve generates the frontier itself and, from 2^20 records up, hands a
         // coarser one to the workers to be deepened on their devices (no host copy of
         // the full frontier, no H2D of it). Same totals, nodes and log lines.
         detail::check_execute_options(n, pre_rows, opts);

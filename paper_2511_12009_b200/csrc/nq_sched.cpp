@@ -177,7 +177,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
   if (!out) return set_error(NQ_ECONFIG, "null report");
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
-  o.strategy = NQ_PARTITION_STRIDED;
+  o.strategy = NQ_PARTITION_GUIDED;  // opts == NULL: dynamic dispatch (one streaming launch per device)
   if (opts) o = *opts;
   if (o.dispatch) {  // a shared dispenser fixes the policy for every cooperating caller
     uint64_t d_count = 0;
@@ -497,7 +497,7 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   if (!out) return set_error(NQ_ECONFIG, "null report");
   nq_solve_opts o{};
   o.variant = NQ_VARIANT_LASTROW;
-  o.strategy = NQ_PARTITION_STRIDED;
+  o.strategy = NQ_PARTITION_GUIDED;  // opts == NULL: dynamic dispatch (one streaming launch per device)
   if (opts) o = *opts;
   if (n < 1 || n > 32)
     return set_error(NQ_ECONFIG, "board size must be in [1, 32], got " + std::to_string(n));
