@@ -454,7 +454,7 @@ def base_line(args, n_gpus, value, t_dev, nodes_per_step, count, clk, launches, 
                    "solutions": OEIS.get(args.n), "nodes_per_step": nodes_per_step,
                    "parallelism": parallelism,
                    "dispatch": "single persistent launch" if args.single_launch else
-                               f"{args.dispatch} host-side dynamic chunks, 2 launches in flight per GPU",
+                               f"{args.dispatch} host-side dynamic chunks fed into one streaming launch per GPU",
                    "l2": "flushed between steps (256 MiB write per GPU, untimed)"},
         "wall_ms": t_dev / args.steps,
         "gpu_launches": launches,

@@ -271,6 +271,9 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.q_pub = c->h_mbox;
   P.q_progress = c->h_mbox ? c->h_mbox + 1 : nullptr;
   P.q_pub_mirror = c->d_ctl + 9;
+  P.watchdog_ns = kQueueWatchdogNs;
+  if (const char* e = std::getenv("NQB_STREAM_WATCHDOG_S"))
+    P.watchdog_ns = static_cast<unsigned long long>(std::atof(e) * 1e9);
   NQ_CUDA(cudaEventRecord(c->ev_k0, c->stream));
   if (count > 0 || c->stream_open) {
     L.fn<<<L.grid, L.block, L.smem, c->stream>>>(P);
@@ -316,9 +319,9 @@ int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
   if (t[6] != 0)
     return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits (multiplier-weighted sum)");
   if (t[7] != 0)
-    return set_error(NQ_ECUDA, "streaming launch: no chunk was published for " +
-                                   std::to_string(kQueueWatchdogNs / 1000000000ull) +
-                                   " s (host side stalled); the launch gave up");
+    return set_error(NQ_ECUDA, "streaming launch: the host published nothing new for the "
+                                "watchdog period (NQB_STREAM_WATCHDOG_S, default 120 s); the "
+                                "launch gave up");
   nq_result r{};
   r.solutions = t[0];
   r.raw_solutions = t[1];

@@ -66,6 +66,7 @@ struct DfsParams {
   const unsigned long long* q_pub;             // mapped host publish word
   unsigned long long* q_progress;              // mapped host: cursor, coarsely
   unsigned long long* q_pub_mirror;            // device: newest publish word any warp read
+  unsigned long long watchdog_ns;              // give up after this long without a publish
 };
 
 // One published chunk of a streaming launch (16-byte aligned: the device mirror is
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           unsigned long long now;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
           if (wait_since == 0ull) wait_since = now;
-          if (now - wait_since > kQueueWatchdogNs) {  // the host stopped publishing
+          if (now - wait_since > P.watchdog_ns) {  // the host stopped publishing
             atomicExch(P.totals + 7, 1ull);
             ticket = kNoTicket;
             exhausted = true;

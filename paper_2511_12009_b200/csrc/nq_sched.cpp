@@ -330,6 +330,13 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
       // from the dispenser while it runs (ctx_stream_*): the GPU never drains between
       // chunks, and the host keeps only a small lead of published-but-untaken records
       // (low_water) so that the last chunks still balance across devices.
+      static const bool dbg = std::getenv("NQB_STREAM_DEBUG") != nullptr;
+      auto trace = [&](const char* what, uint64_t a = 0, uint64_t b = 0) {
+        if (!dbg) return;
+        const double t = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        std::fprintf(stderr, "[%9.3f ms] worker %d: %s %llu %llu\n", t, w, what,
+                     static_cast<unsigned long long>(a), static_cast<unsigned long long>(b));
+      };
       auto stream_worker = [&](int wk, nq_ctx* c, nq_worker_stats& ws) -> int {
         struct Pushed {
           uint64_t vstart, first, len;
@@ -341,8 +348,10 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         const nq_sub* all = src;
         uint64_t all_n = count;
         int e = NQ_OK;
+        trace("prepare", count);
         if (kind == kLaunchHost) e = ctx_upload(c, src, count, &all);
         else if (kind == kLaunchExpand) e = ctx_deepen(c, n, target_rows, src, count, &all, &all_n);
+        trace("resident", all_n);
         if (e == NQ_OK && all_n != disp_count)
           e = set_error(NQ_ECONFIG, "deepened batch has " + std::to_string(all_n) +
                                         " records, the dispenser " + std::to_string(disp_count));
@@ -353,38 +362,60 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         const uint64_t lanes = ctx_lanes(c, n, launch_rows);
         const uint64_t low_water = std::max<uint64_t>(lanes / 8, 4096);
         if (e == NQ_OK) e = ctx_stream_begin(c, max_chunks);
-        if (e == NQ_OK) e = ctx_stream_launch(c, n, launch_rows, o.variant);
+        trace("begun", max_chunks, lanes);
         if (e) {
           if (kind == kLaunchExpand) ctx_release_deep(c);
           return e;
         }
+        // The feeder runs on its own thread and makes NO CUDA call: this thread's launch
+        // (and anything after it) can block on driver locks held by another thread that
+        // is synchronising the device — i.e. waiting for this very kernel, which only
+        // ends once the feeder has published everything and closed the queue.
+        std::atomic<bool> launch_failed{false};
         bool cancelled = false;
-        while (e == NQ_OK) {
-          if (cancel_raised(o.cancel)) {
-            cancelled = true;
-            interrupted.store(true);
-            break;
+        int fe = NQ_OK;
+        std::string fe_msg;  // nq_last_error() is per thread: carried back to this one
+        std::thread feeder([&] {
+          while (fe == NQ_OK && !launch_failed.load()) {
+            if (cancel_raised(o.cancel)) {
+              cancelled = true;
+              interrupted.store(true);
+              break;
+            }
+            uint64_t consumed = 0;
+            ctx_stream_consumed(c, &consumed);
+            const uint64_t pub = ctx_stream_published(c);
+            if (pub - consumed >= low_water) {
+              std::this_thread::sleep_for(std::chrono::microseconds(20));
+              continue;
+            }
+            uint64_t f = 0, l = 0;
+            const int got = nq_dispatch_take(disp, &f, &l);
+            if (got < 0) {
+              fe = got;
+              break;
+            }
+            if (got == 0) break;  // dispenser drained: close the queue below
+            pushed.push_back(Pushed{pub, f, l});
+            fe = ctx_stream_push(c, all + f, l);
+            trace("published", f, l);
           }
-          uint64_t consumed = 0;
-          ctx_stream_consumed(c, &consumed);
-          const uint64_t pub = ctx_stream_published(c);
-          if (pub - consumed >= low_water) {
-            std::this_thread::sleep_for(std::chrono::microseconds(20));
-            continue;
-          }
-          uint64_t f = 0, l = 0;
-          const int got = nq_dispatch_take(disp, &f, &l);
-          if (got < 0) {
-            e = got;
-            break;
-          }
-          if (got == 0) break;  // dispenser drained: close the queue below
-          pushed.push_back(Pushed{pub, f, l});
-          e = ctx_stream_push(c, all + f, l);
+          if (fe != NQ_OK) fe_msg = nq_last_error();
+          ctx_stream_close(c, cancelled || fe != NQ_OK);
+          trace("closed", ctx_stream_published(c));
+        });
+        e = ctx_stream_launch(c, n, launch_rows, o.variant);
+        trace("launched", e);
+        if (e) launch_failed.store(true);
+        feeder.join();
+        if (e) {
+          if (kind == kLaunchExpand) ctx_release_deep(c);
+          return e;
         }
-        ctx_stream_close(c, cancelled || e != NQ_OK);
+        e = fe == NQ_OK ? NQ_OK : set_error(fe, fe_msg);
         nq_result r{};
         const int re = nq_collect(c, &r);  // always drain the launch
+        trace("collected", re, r.subproblems);
         if (kind == kLaunchExpand) ctx_release_deep(c);
         ws.launches += 1;
         ws.chunks += pushed.size();
