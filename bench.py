@@ -386,7 +386,7 @@ def run_single_process(args):
     line = base_line(args, G, value, t_dev, nodes_per_step, count, clk, launches,
                      "1 process, one host thread per GPU" if G > 1 else "1 GPU")
     line["roofline"] = roofline(value / G, nodes_per_step // G, 0)
-    line["roofline"]["traffic"] = ncu_traffic(args.n, args.pre_rows) if G == 1 and ctx else None
+    line["roofline"]["traffic"] = ncu_traffic(args.n, args.pre_rows) if G == 1 else None
     line["device_ms_per_step"] = dev_ms
 
     if not args.no_e2e:
