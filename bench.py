@@ -19,8 +19,8 @@ the host with checked adds. No NCCL anywhere:
 
 value  — frontier resident in HBM on every GPU (replicated, copied before timing), CUDA
          events: per GPU, first enqueued launch -> end of its last kernel; max over GPUs.
-e2e    — nq_solve_batch with the frontier in pinned HOST memory: every chunk is copied
-         H2D by the GPU that takes it, results D2H; host wall clock, max over ranks.
+e2e    — nq_solve_batch with the frontier in pinned HOST memory: one H2D of the frontier
+         per GPU, the streaming count, results D2H; host wall clock, max over ranks.
 roofline — integer-issue bound: achieved = per-GPU nodes/s x 18 algorithmic int ops per
            node vs the int-op peak measured live (nq_measure_int_peak).
 cpu_baseline — the reference's execute_batch (oracle/_ref/libnqref.so, built from the
@@ -403,12 +403,14 @@ def run_single_process(args):
             wall.append((time.perf_counter() - t0) * 1e3)
             check_total(args.n, rep.total, "e2e step")
         line["e2e"] = {"value": nodes_per_step * args.steps / (sum(wall) / 1e3), "unit": "nodes/s",
-                       "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": 80 * sum(
+                       # every GPU uploads the whole frontier once (dynamic dispatch may give
+                       # it any record), then counts the chunks it takes
+                       "h2d_bytes_per_step": count * 16 * G, "d2h_bytes_per_step": 80 * sum(
                            w.launches for w in workers_of(rep)),
                        "ms_per_step": sum(wall) / args.steps,
                        "call": f"nq_solve_batch (execute_batch) on the pinned host frontier, "
-                               f"{args.dispatch} dispatch over {G} GPU(s); every chunk H2D by the "
-                               f"GPU that takes it; host wall clock"}
+                               f"{args.dispatch} dispatch over {G} GPU(s): one H2D of the frontier "
+                               f"per GPU, streaming count, result read-back; host wall clock"}
     if not args.no_execute:
         rep = None
         for _ in range(2):  # the first call also maps the stream-ordered pool; report the second
@@ -563,12 +565,12 @@ def run_torchrun(args):
         line["device_ms_per_step"] = step_ms
         if e2e is not None:
             line["e2e"] = {"value": nodes_per_step * args.steps / (sum(e2e[0]) / 1e3),
-                           "unit": "nodes/s", "h2d_bytes_per_step": count * 16,
+                           "unit": "nodes/s", "h2d_bytes_per_step": count * 16 * world,
                            "d2h_bytes_per_step": 80 * e2e[1],
                            "ms_per_step": sum(e2e[0]) / args.steps,
-                           "call": "nq_solve_batch per rank on the pinned host frontier, chunks "
-                                   "from the shared dispenser, H2D by the GPU that takes them; "
-                                   "host wall clock incl. the barriers, max over ranks"}
+                           "call": "nq_solve_batch per rank on the pinned host frontier (one H2D "
+                                   "per GPU), chunks from the shared dispenser; host wall clock "
+                                   "incl. the barriers, max over ranks"}
         print(json.dumps(line))
     disp.close(unlink=False)
     dist.destroy_process_group()
