@@ -281,41 +281,38 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
       const std::string range_name = "nq_solve_batch worker " + std::to_string(w);
       NvtxRange range(range_name.c_str());
       const auto s0 = clk::now();
-      nq_ctx* cx[2] = {nullptr, nullptr};  // [0]: this worker's context
+      nq_ctx* c0 = nullptr;                   // this worker's context
       struct Flight {
-        bool busy = false;
         uint64_t first = 0, len = 0, work = 0;
-      } fl[2];
+      } fl;                                   // the one-launch strategies' launch
       uint64_t bad_first = 0, bad_len = 0;  // the launch that failed (for the message)
       uint64_t bad_record = ~0ull;           // streaming: the rejected record's batch index
       bool strided_index = false;
-      int rc = pooled_ctx(st.device, slot[w], &cx[0]);
-      for (nq_ctx* c : cx)
-        if (c) nq_ctx_set_cancel(c, o.cancel);
-      if (rc == NQ_OK) rc = ctx_mark_start(cx[0]);
-      auto launch = [&](int i, const nq_sub* base, uint64_t f, uint64_t l) -> int {
-        const int e = ctx_launch(cx[i], n, launch_rows, o.variant, base + f, l, kind);
+      int rc = pooled_ctx(st.device, slot[w], &c0);
+      if (rc == NQ_OK) nq_ctx_set_cancel(c0, o.cancel);
+      if (rc == NQ_OK) rc = ctx_mark_start(c0);
+      // uniform / weighted / strided: one launch over this worker's records, then collect
+      auto launch = [&](const nq_sub* base, uint64_t f, uint64_t l) -> int {
+        const int e = ctx_launch(c0, n, launch_rows, o.variant, base + f, l, kind);
         if (e) {
           bad_first = f;
           bad_len = l;
           return e;
         }
-        fl[i].busy = true;
-        fl[i].first = f;
-        fl[i].len = l;
-        fl[i].work = kind == kLaunchExpand ? ctx_last_expanded(cx[i]) : l;
+        fl.first = f;
+        fl.len = l;
+        fl.work = kind == kLaunchExpand ? ctx_last_expanded(c0) : l;
         return NQ_OK;
       };
-      auto collect = [&](int i) -> int {
+      auto collect = [&]() -> int {
         nq_result r{};
-        fl[i].busy = false;
-        const int e = nq_collect(cx[i], &r);
+        const int e = nq_collect(c0, &r);
         if (e) {
-          bad_first = fl[i].first;
-          bad_len = fl[i].len;
+          bad_first = fl.first;
+          bad_len = fl.len;
           return e;
         }
-        if (r.subproblems < fl[i].work) interrupted.store(true);  // cancelled inside the launch
+        if (r.subproblems < fl.work) interrupted.store(true);  // cancelled inside the launch
         if (!add_ok(st.partial_sum, r.solutions, &st.partial_sum))
           return set_error(NQ_EOVERFLOW, "solution count overflows 64 bits");
         st.processed += r.subproblems;
@@ -323,7 +320,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         st.chunks += 1;
         st.launches += 1;
         st.kernel_ms += r.kernel_ms;
-        st.span_ms = std::max(st.span_ms, ctx_span_ms(cx[0], cx[i]));
+        st.span_ms = std::max(st.span_ms, ctx_span_ms(c0, c0));
         return NQ_OK;
       };
       // Dynamic strategies: ONE persistent streaming launch per worker, fed chunk by chunk
@@ -438,7 +435,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         ws.processed += r.subproblems;
         ws.nodes += r.nodes;
         ws.kernel_ms += r.kernel_ms;
-        ws.span_ms = std::max(ws.span_ms, ctx_span_ms(cx[0], c));
+        ws.span_ms = std::max(ws.span_ms, ctx_span_ms(c0, c));
         (void)wk;
         return NQ_OK;
       };
@@ -462,8 +459,8 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (mine_n) {
-            rc = launch(0, mine, 0, mine_n);
-            if (rc == NQ_OK) rc = collect(0);
+            rc = launch(mine, 0, mine_n);
+            if (rc == NQ_OK) rc = collect();
           }
         } else if (!ranges.empty()) {
           const uint64_t first = ranges[2 * w], len = ranges[2 * w + 1] - first;
@@ -472,23 +469,20 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (len) {
-            rc = launch(0, src, first, len);
-            if (rc == NQ_OK) rc = collect(0);
+            rc = launch(src, first, len);
+            if (rc == NQ_OK) rc = collect();
           }
         } else {
           emit(o, NQ_LOG_START, w, 0, 0.0);
-          rc = stream_worker(w, cx[0], st);
+          rc = stream_worker(w, c0, st);
         }
       }
       st.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - s0).count();
-      for (nq_ctx* c : cx)
-        if (c) nq_ctx_set_cancel(c, nullptr);
+      if (c0) nq_ctx_set_cancel(c0, nullptr);
       if (rc) {
         std::lock_guard<std::mutex> lk(fail_mu);
         if (failure.empty()) {
-          uint64_t bad = ~0ull;
-          for (nq_ctx* c : cx)
-            if (c && ctx_last_bad(c) != ~0ull) bad = ctx_last_bad(c);
+          uint64_t bad = c0 ? ctx_last_bad(c0) : ~0ull;
           uint64_t global_bad = strided_index
                                     ? static_cast<uint64_t>(w) + bad * static_cast<uint64_t>(W)
                                     : bad_first + bad;

@@ -428,12 +428,14 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
   CHECK(one.total == 1 && one.workers.size() == 1);
   CHECK(execute(18, 6, ExecuteOptions{}).total == 666090624ull);
 
-  // strided plans go through nq_solve: N=16 R=7 (1 999 228 records >= 2^20) is dealt as
-  // the R=4 frontier and deepened on the device; N=10 stays on the host frontier.
+  // guided and strided plans go through nq_solve: N=16 R=7 (1 999 228 records >= 2^20) is
+  // dealt as the R=4 frontier and deepened on the device; N=10 stays on the host frontier.
+  // guided: one streaming launch per worker, fed chunk by chunk from the dispenser.
+  for (auto strat : {PartitionStrategy::strided, PartitionStrategy::guided})
   for (int w : {1, 3}) {
     std::vector<std::string> slines;
     ExecuteOptions s;
-    s.plan.strategy = PartitionStrategy::strided;
+    s.plan.strategy = strat;
     s.plan.worker_count = w;
     s.log = [&](const std::string& l) {
       std::lock_guard<std::mutex> lk(mu);
@@ -441,8 +443,11 @@ void execute_cases() {  // test_scheduler.cpp:77-171, acceptance.cpp:60-75
     };
     const auto srep = execute(16, 7, s);
     CHECK(srep.completed && srep.total == 14772512ull);
+    CHECK(srep.nodes == 560708278ull);  // SURVEY Appendix B, N=16 R=7
     CHECK(srep.task_count == count_subproblems(16, 7));
     CHECK(static_cast<int>(srep.workers.size()) == w);
+    if (strat == PartitionStrategy::guided)
+      for (const auto& ws : srep.workers) CHECK(ws.launches == 1);
     std::uint64_t sp = 0;
     for (const auto& ws : srep.workers) sp += ws.processed;
     CHECK(sp == srep.task_count);

@@ -238,10 +238,12 @@ def test_empty_and_rejected_batches():
     with pytest.raises(_lib.NqError):
         ctx.count(10, 3, shallow)  # placed_rows below the declared pre_rows
     ctx.close()
-    for strategy in (nq.PartitionStrategy.uniform, nq.PartitionStrategy.strided):
-        opts = nq.ExecuteOptions(plan=nq.PartitionPlan(strategy, 2))
+    for strategy in (nq.PartitionStrategy.uniform, nq.PartitionStrategy.strided,
+                     nq.PartitionStrategy.guided, nq.PartitionStrategy.stealing):
+        opts = nq.ExecuteOptions(plan=nq.PartitionPlan(strategy, 2, [], 16))
         with pytest.raises(RuntimeError) as e:
             nq.execute_batch(10, 3, bad, opts)
+        # streaming launches report the queue position; the scheduler maps it back
         assert "failed on subproblem 5" in str(e.value), (strategy, str(e.value))
 
 
