@@ -185,8 +185,8 @@ typedef void (*nq_log_fn)(void* user, const char* line);
  * its own; a NAMED dispenser lives in a POSIX shared-memory segment, so that cooperating
  * processes on one node (e.g. one per GPU under torchrun) share ONE dynamic dispatch —
  * host-side, lock-free, no device collective. strategy: NQ_PARTITION_STEALING (fixed
- * chunks, stream order) or NQ_PARTITION_GUIDED (max(remaining / 2W, floor) records from
- * the expensive end; chunk = floor, 0 = count / (128 W)). Each process posts its partial
+ * chunks, stream order) or NQ_PARTITION_GUIDED (max(min(remaining / 2W, count / 16W),
+ * floor) records from the expensive end; chunk = floor, 0 = count / (128 W)). Each process posts its partial
  * into its own slot; nq_dispatch_sum adds the slots (checked). */
 typedef struct nq_dispatch nq_dispatch;
 int nq_dispatch_create(const char* shm_name /* NULL = in-process */, uint64_t count, int strategy,

@@ -6,9 +6,9 @@
 // GPU (torchrun) draws from one dispenser: still host-side, lock-free dynamic dispatch,
 // with no device collective. Two policies:
 //   stealing  fixed chunks in stream order (the reference's),
-//   guided    max(remaining / 2W, floor) records from the EXPENSIVE end of the stream
-//             (a record's cost rises with its index): big chunks first,
-//             small ones at the end, so the devices finish together.
+//   guided    max(min(remaining / 2W, count / 16W), floor) records from the EXPENSIVE
+//             end of the stream (a record's cost rises with its index):
+//             big chunks first, small ones at the end, so the devices finish together.
 // Each process posts its partial (solutions, nodes, records) into its own slot; the
 // host sums the slots with checked 64-bit adds (scheduler.hpp:384-386).
 #include <fcntl.h>
@@ -71,8 +71,8 @@ int init_shared(Shared* s, uint64_t count, int strategy, uint64_t chunk, int wor
   s->count = count;
   s->strategy = strategy;
   s->workers = workers;
-  // guided floor: small enough that the last chunks even out the devices, large
-  // enough that the launch cost (~20 us, hidden by double buffering) stays negligible.
+  // guided floor: small enough that the last chunks even out the devices; a streaming
+  // launch takes chunks of any size without a launch or a tail per chunk.
   s->chunk = chunk ? chunk : std::max<uint64_t>(count / (128ull * workers), 1);
   s->taken.store(0);
   s->epoch.store(0);
@@ -172,11 +172,18 @@ int nq_dispatch_take(nq_dispatch* d, uint64_t* first, uint64_t* len) {
     *len = std::min(s->chunk, count - f);
     return 1;
   }
+  // Guided, capped: max(min(remaining / 2W, count / 16W), floor). The records are taken
+  // from the expensive end, where one record costs several times the average (N=22: the
+  // last 1/16 of the stream holds ~1/5 of the work), so an uncapped first chunk of
+  // count / 2W records would be more than one GPU's whole share.
+  const uint64_t cap = std::max<uint64_t>(count / (16ull * s->workers), s->chunk);
   uint64_t t = s->taken.load(std::memory_order_relaxed);
   for (;;) {
     if (t >= count) return 0;
     const uint64_t rem = count - t;
-    const uint64_t sz = std::min(rem, std::max<uint64_t>(rem / (2ull * s->workers), s->chunk));
+    const uint64_t sz =
+        std::min<uint64_t>(rem, std::max<uint64_t>(std::min<uint64_t>(rem / (2ull * s->workers), cap),
+                                                   s->chunk));
     if (s->taken.compare_exchange_weak(t, t + sz, std::memory_order_relaxed)) {
       *first = count - t - sz;  // from the back: the expensive end first
       *len = sz;

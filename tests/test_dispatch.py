@@ -49,7 +49,9 @@ def test_guided_covers_every_record_once_expensive_end_first(count, workers):
         assert firsts == sorted(firsts, reverse=True)   # then walks toward the cheap front
         sizes = [n for _, n in chunks]
         assert all(a >= b for a, b in zip(sizes, sizes[1:]) if b >= info["chunk"])
-        assert sizes[0] == max(count // (2 * workers), min(count, info["chunk"]))
+        cap = max(count // (16 * workers), info["chunk"])
+        assert sizes[0] == min(count, max(min(count // (2 * workers), cap), info["chunk"]))
+        assert max(sizes) <= max(cap, 1)        # no chunk larger than 1/16 of a worker's share
 
 
 def test_stealing_is_the_reference_cursor():
