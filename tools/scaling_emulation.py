@@ -14,7 +14,12 @@ operation -> end of its kernel). Caveat: when a virtual GPU runs dry its blocks 
 the SMs and the remaining workers' blocks get a larger share of each SM, which a real
 idle GPU would not give them; the emulated end-phase imbalance is therefore a lower bound.
 
-    python tools/scaling_emulation.py --n 20 --pre-rows 7 --ks 1,2,4,8
+    python tools/scaling_emulation.py --n 20 --pre-rows 7 --ks 1,2,4,8            # 8 blocks/SM
+    python tools/scaling_emulation.py --n 22 --pre-rows 7 --ks 1,7 --blocks 7     # 7 blocks/SM
+
+--blocks must be the one-GPU occupancy of the workload (the stack depth sets it: 8 blocks
+per SM at N=20 R=7, 7 at N=22 R=7), and k must divide it: otherwise one virtual GPU's
+launch cannot be resident next to the others and only starts when one of them ends.
 """
 from __future__ import annotations
 
@@ -63,6 +68,9 @@ def main():
         return
     t1 = None
     for k in [int(x) for x in args.ks.split(",")]:
+        if args.blocks % k:
+            raise SystemExit(f"k={k} does not divide --blocks {args.blocks}: the k launches "
+                             f"would not all be resident at once")
         # enough hardware queues for k concurrent persistent launches on one device
         env = {**os.environ, "NQB_BLOCKS_PER_SM": str(max(1, args.blocks // k)),
                "CUDA_DEVICE_MAX_CONNECTIONS": "32"}
