@@ -433,10 +433,14 @@ int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks) {
 
 int ctx_stream_launch(nq_ctx* c, int n, int pre_rows, int variant) {
   if (!c || !c->stream_open) return set_error(NQ_ECONFIG, "no streaming launch begun");
-  if (int rc = check_args(n, pre_rows, variant)) return rc;
-  NQ_CUDA(cudaSetDevice(c->device));
-  if (int rc = enqueue(c, n, pre_rows, variant, nullptr, 0, false, nullptr, nullptr, nullptr))
+  int rc = check_args(n, pre_rows, variant);
+  if (rc == NQ_OK && cudaSetDevice(c->device) != cudaSuccess)
+    rc = set_error(NQ_ECUDA, "cudaSetDevice failed");
+  if (rc == NQ_OK) rc = enqueue(c, n, pre_rows, variant, nullptr, 0, false, nullptr, nullptr, nullptr);
+  if (rc) {  // nothing is running: the next launch on this context is a plain one again
+    c->stream_open = false;
     return rc;
+  }
   c->pending = true;
   c->p_variant = variant;
   c->p_h2d = false;
