@@ -155,3 +155,25 @@ def test_soft_stop_records_every_started_chunk(tmp_path):
     assert sum(w.processed for w in first.workers) == sum(sizes[chunks - done:])
     rest = nq.execute_checkpointed(19, 6, nq.ExecuteOptions(), p, chunk=100000, resume=True)
     assert rest.completed and rest.total == 4968057848
+
+
+def test_cli_resume_takes_kernel_and_chunk_from_the_file(tmp_path):
+    """`resume FILE` re-applies the run's kernel variant and chunk (both part of the
+    file's identity): an ITERATIVE-kernel checkpoint with a custom chunk resumes, and the
+    new worker / device options are accepted. Every chunk is recorded, so no GPU runs."""
+    import subprocess
+    import sys
+    n, r, chunk = 12, 4, 700
+    tasks = nq.count_subproblems(n, r)
+    k = (tasks + chunk - 1) // chunk
+    done = {i: (14200 // k + (1 if i < 14200 % k else 0), 3) for i in range(k)}
+    p = tmp_path / "it.ckpt"
+    write_ckpt(p, n, r, 0, chunk, tasks, done)
+    d = nq.checkpoint_details(p)
+    assert (d["kernel"], d["chunk"], d["chunks"], d["done_chunks"]) == (nq.KernelVariant.iterative, chunk, k, k)
+    out = subprocess.run([sys.executable, "-m", "paper_2511_12009_b200.cli", "resume", str(p),
+                          "--workers", "2", "--format", "json"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "kernel=iterative" in out.stderr and f"chunk={chunk}" in out.stderr
+    assert '"total": 14200' in out.stdout

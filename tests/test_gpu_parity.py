@@ -461,3 +461,27 @@ def test_tail_donation_keeps_every_count_and_balances(golden):
         if r == 3:  # a from-the-root split: Alg. 3 nodes from R=3 = R=5 count + rows 4, 5
             want = golden["appendix_b_nodes"]["18"]["5"] + nq.count_subproblems(18, 4) + nq.count_subproblems(18, 5)
             assert outs[1][2] == want
+
+
+def test_deepening_through_an_all_dead_level():
+    """A root whose next level has records but whose level after that has none (n=5, two
+    rows placed): deepening to 4 rows yields zero records, and counting through the
+    deepening paths returns 0 instead of launching empty grids (round-1 ADVICE)."""
+    import torch
+    root = np.array([(17, 36, 8, 514)], dtype=np.uint32).view(_lib.SUB_DTYPE).reshape(-1)
+    assert len(nq.expand(5, root, 3)) == 1 and len(nq.expand(5, root, 4)) == 0
+    dev = torch.from_numpy(root.view(np.int32).reshape(-1, 4)).cuda()
+    total = ctypes.c_uint64()
+    _lib.check(_lib.lib.nq_expand_device(0, 5, ctypes.c_void_p(dev.data_ptr()), 1, 4, None, 0,
+                                         ctypes.byref(total)))
+    assert total.value == 0
+    c = Ctx()
+    r = _lib.NqResult()
+    _lib.check(_lib.lib.nq_count_expand(c.p, 5, 4, _lib.VARIANT_LASTROW, root.ctypes.data, 1,
+                                        ctypes.byref(r)))
+    assert r.solutions == 0 and r.subproblems == 0
+    c.close()
+    for strategy in (nq.PartitionStrategy.strided, nq.PartitionStrategy.guided):
+        rep = nq.execute_batch_expand(5, 4, root, nq.ExecuteOptions(
+            config=CFG1, plan=nq.PartitionPlan(strategy, 2)))
+        assert rep.total == 0 and rep.completed
