@@ -266,11 +266,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   // published by the host) and a monotone hint into the chunk table
   unsigned long long ticket = kNoTicket;
   uint32_t chunk = 0u;
-  unsigned long long wait_since = 0ull;
   unsigned long long pub_seen = 0ull;  // warp-uniform: published positions last read
   bool closed_seen = false;
-  const uint4* chunk_base = nullptr;   // this lane's cached chunk entry (end 0: none)
-  unsigned long long chunk_end = 0ull;
 
   // Starts record `idx` (reported as the failing index) at `rec` on this lane.
   // Streaming chunks are copied in while the kernel runs, so their records are read
@@ -307,6 +304,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
     // ---- refill idle lanes (once per KSTEP block) ----------------------------------
     uint32_t idle = __ballot_sync(0xffffffffu, a == 0u);
     if (idle) {
+      unsigned long long wait_since = 0ull;  // streaming: start of the current nap
       for (;;) {
         if (a == 0u && busy) {  // fold the finished record (or donated piece of one)
           const unsigned long long prod = static_cast<unsigned long long>(weight) * sol;  // < 2^56
@@ -398,9 +396,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
         if (ticket != kNoTicket) {
           if (ticket < pub_seen) {
             // chunk lookup: the device mirror, filled from the host table on a miss
-            unsigned long long eb = reinterpret_cast<unsigned long long>(chunk_base), ee = chunk_end;
-            while (ticket >= ee) {  // tickets only grow: move to the entry holding this one
-              if (ee != 0ull) ++chunk;
+            unsigned long long eb, ee;
+            for (;; ++chunk) {  // tickets only grow: move to the entry holding this one
               asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(eb), "=l"(ee)
                            : "l"(P.q_tab + chunk) : "memory");
               if (ee == 0ull) {  // first reader of this entry: fetch it from the host table
@@ -411,9 +408,8 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
                 asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + chunk), "l"(eb),
                              "l"(ee) : "memory");
               }
+              if (ticket < ee) break;
             }
-            chunk_base = reinterpret_cast<const uint4*>(eb);
-            chunk_end = ee;
             // expensive end of the chunk first, like the contiguous launch (reverse)
             start(reinterpret_cast<const uint4*>(eb) + (ee - 1ull - ticket), ticket);
             ticket = kNoTicket;
@@ -438,7 +434,6 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           __nanosleep(1000);
           continue;
         }
-        wait_since = 0ull;
         break;
       }
       if constexpr (!PER_SUB) {
