@@ -83,9 +83,28 @@ KernelFn pick(bool per_sub, int layout) {
 
 // n = 32: candidate sets can use bit 31; one V4 instantiation at 128 threads carries the
 // adjusted node counter (nq_kernel.cuh, WIDE).
-KernelFn wide_kernel(bool per_sub) {
+KernelFn wide_kernel(bool per_sub, bool stream) {
+  if (stream) return nq_dfs_kernel<128, kStep, false, kLayoutV4, true, true>;
   return per_sub ? nq_dfs_kernel<128, kStep, true, kLayoutV4, true>
                  : nq_dfs_kernel<128, kStep, false, kLayoutV4, true>;
+}
+
+// Streaming launches (records from the host-published queue): no per-record outputs.
+template <int B>
+KernelFn pick_stream(int layout) {
+  return layout == NQ_LAYOUT_PLANES ? nq_dfs_kernel<B, kStep, false, kLayoutPlanes, false, true>
+                                    : nq_dfs_kernel<B, kStep, false, kLayoutV4, false, true>;
+}
+
+KernelFn stream_kernel_for(int block, int layout) {
+  switch (block) {
+    case 64: return pick_stream<64>(layout);
+    case 96: return pick_stream<96>(layout);
+    case 128: return pick_stream<128>(layout);
+    case 192: return pick_stream<192>(layout);
+    case 256: return pick_stream<256>(layout);
+    default: return nullptr;
+  }
 }
 
 KernelFn kernel_for(int block, bool per_sub, int layout) {
@@ -175,15 +194,16 @@ int set_kernel_attributes(int device) {
   for (int block : {64, 96, 128, 192, 256})
     for (bool per_sub : {false, true})
       for (int layout : {NQ_LAYOUT_V4, NQ_LAYOUT_PLANES}) {
-        KernelFn fn = kernel_for(block, per_sub, layout);
-        NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-        NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        KernelFn fns[2] = {kernel_for(block, per_sub, layout), stream_kernel_for(block, layout)};
+        for (KernelFn fn : fns) {
+          NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+          NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
       }
-  for (bool per_sub : {false, true}) {
-    NQ_CUDA(cudaFuncSetAttribute(wide_kernel(per_sub), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 optin));
-    NQ_CUDA(cudaFuncSetAttribute(wide_kernel(per_sub),
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  for (int k = 0; k < 3; ++k) {
+    KernelFn fn = wide_kernel(k == 1, k == 2);
+    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
   done[device] = true;
   return NQ_OK;
@@ -200,7 +220,9 @@ int plan_launch(nq_ctx* c, int n, int pre_rows, bool per_sub, Launch* L) {
   const int frames = std::max(n - 1 - pre_rows, 0);
   const int levels = frames + 1;  // + the idle sentinel
   L->block = n >= 32 ? 128 : c->block;
-  L->fn = n >= 32 ? wide_kernel(per_sub) : kernel_for(c->block, per_sub, c->layout);
+  L->fn = n >= 32 ? wide_kernel(per_sub, c->stream_open)
+                  : c->stream_open ? stream_kernel_for(c->block, c->layout)
+                                   : kernel_for(c->block, per_sub, c->layout);
   if (!L->fn) return set_error(NQ_ECONFIG, "unsupported block size " + std::to_string(c->block));
   L->smem = static_cast<size_t>(levels) * L->block * 16u;
   int per_sm = 0;

@@ -228,9 +228,12 @@ __device__ __forceinline__ void dfs_step(uint32_t& C, uint32_t& l, uint32_t& r, 
   }
 }
 
-template <int BLOCK, int KSTEP, bool PER_SUB, int LAYOUT, bool WIDE = false>
-__global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
+// STREAM: records come from the host-published chunk queue (P.stream must be set);
+// a separate instantiation, so the contiguous launch carries none of its state.
+template <int BLOCK, int KSTEP, bool PER_SUB, int LAYOUT, bool WIDE = false, bool STREAM = false>
+__global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P) {
   static_assert(!WIDE || LAYOUT == kLayoutV4, "n = 32 runs the V4 layout");
+  static_assert(!(STREAM && PER_SUB), "per-record outputs use the contiguous launch");
   extern __shared__ uint4 stk[];  // [levels][BLOCK] frames (or [levels][4][BLOCK] words)
   constexpr uint32_t STRIDE = BLOCK * 16u;
   const uint32_t lane = threadIdx.x & 31u;
@@ -273,7 +276,9 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
   // Streaming chunks are copied in while the kernel runs, so their records are read
   // through L2 (ld.global.cg), never from a possibly stale non-coherent line.
   auto start = [&](const uint4* rec, unsigned long long idx) {
-    const uint4 s = P.stream ? __ldcg(rec) : __ldg(rec);
+    uint4 s;
+    if constexpr (STREAM) s = __ldcg(rec);
+    else s = __ldg(rec);
     busy = true;
     weight = s.w >> 8;
     placed = static_cast<int>(s.w & 0xffu);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           busy = false;
         }
         if (exhausted) break;
-        if (!P.stream) {
+        if constexpr (!STREAM) {
           const uint32_t need = __ballot_sync(0xffffffffu, a == 0u);
           if (need == 0u) break;
           const uint32_t leader = __ffs(need) - 1u;
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
             }
           }
           continue;
-        }
+        } else {
         // Streaming: (1) idle lanes without a queue position take one from the cursor,
         const uint32_t need = __ballot_sync(0xffffffffu, a == 0u && ticket == kNoTicket);
         unsigned long long taken_end = 0ull;
@@ -435,6 +440,7 @@ __global__ void __launch_bounds__(BLOCK) nq_dfs_kernel(DfsParams P) {
           continue;
         }
         break;
+        }  // STREAM
       }
       if constexpr (!PER_SUB) {
         // Tail balancing inside the warp. Once the queue is empty, an idle lane takes
