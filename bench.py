@@ -284,6 +284,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-execute", action="store_true")
+    ap.add_argument("--no-zero-conflict", action="store_true",
+                    help="skip timing the zero-bank-conflict plane layout beside the default")
     args = ap.parse_args()
     if args.pre_rows is None:
         # R=7: 22.8 M finer subtrees keep every lane busy to the end (lane efficiency
@@ -420,12 +422,37 @@ def run_single_process(args):
                                    "total_ms": rep.generation_ms + rep.calc_ms,
                                    "call": f"nq_solve (execute): coarse frontier on the host, "
                                            f"deepened + counted on {G} GPU(s), {args.dispatch}"}
+    if G == 1 and not args.no_zero_conflict:
+        line["zero_conflict_layout"] = zero_conflict_layout(args, devs[0], count, flush_l2)
     if G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     print(json.dumps(line))
     if ctx is not None:
         _lib.lib.nq_ctx_destroy(ctx)
     return 0
+
+
+def zero_conflict_layout(args, dev, count, flush_l2):
+    """The north star's zero-bank-conflict configuration, timed beside the default: the
+    same count with the 32-bit plane stack (NQ_LAYOUT_PLANES: lane t owns bank t in four
+    word planes), one contiguous launch, checked. Its per-instruction ncu evidence (0
+    excess wavefronts on every LDS/STS at this workload) is profiles/r02_ncu_dfs_planes_n20_r7.md."""
+    from paper_2511_12009_b200 import _lib
+    ctx = ctypes.c_void_p()
+    _lib.check(_lib.lib.nq_ctx_create(0, ctypes.byref(ctx)))
+    _lib.check(_lib.lib.nq_ctx_set_layout(ctx, _lib.LAYOUT_PLANES))
+    try:
+        r = _lib.NqResult()
+        flush_l2()
+        _lib.check(_lib.lib.nq_count_device(ctx, args.n, args.pre_rows, _lib.VARIANT_LASTROW,
+                                            ctypes.c_void_p(dev.data_ptr()), count, ctypes.byref(r)))
+        check_total(args.n, r.solutions, "plane-layout count")
+        return {"layout": "32-bit planes", "ms": r.kernel_ms,
+                "nodes_per_s": r.nodes / (r.kernel_ms * 1e-3),
+                "ncu_excess_smem_wavefronts_per_instruction": 0,
+                "evidence": "profiles/r02_ncu_dfs_planes_n20_r7.md"}
+    finally:
+        _lib.lib.nq_ctx_destroy(ctx)
 
 
 def cpu_baseline(args):
