@@ -162,14 +162,26 @@ void nq_dispatch_close(nq_dispatch* d, int unlink) {
 }
 
 int nq_dispatch_take(nq_dispatch* d, uint64_t* first, uint64_t* len) {
+  return nqb200::dispatch_take_at_least(d, 0, first, len);
+}
+
+}  // extern "C"
+
+// Stealing hands out whole chunks; a streaming feeder that needs `want` records takes
+// ceil(want / chunk) consecutive chunks in ONE step (one contiguous range, one queue
+// entry), the reference's granularity per take but not per queue entry: a chunk of 64
+// records per entry would make every lane walk thousands of entries per record.
+int nqb200::dispatch_take_at_least(nq_dispatch* d, uint64_t want, uint64_t* first,
+                                   uint64_t* len) {
   if (!d || !first || !len) return set_error(NQ_ECONFIG, "null dispenser argument");
   Shared* s = d->s;
   const uint64_t count = s->count;
   if (s->strategy == NQ_PARTITION_STEALING) {  // scheduler.hpp:356-361
-    const uint64_t f = s->taken.fetch_add(s->chunk, std::memory_order_relaxed);
+    const uint64_t k = std::max<uint64_t>((want + s->chunk - 1) / s->chunk, 1);
+    const uint64_t f = s->taken.fetch_add(k * s->chunk, std::memory_order_relaxed);
     if (f >= count) return 0;
     *first = f;
-    *len = std::min(s->chunk, count - f);
+    *len = std::min(k * s->chunk, count - f);
     return 1;
   }
   // Guided, capped: max(min(remaining / 2W, count / 16W), floor). The records are taken
@@ -191,6 +203,8 @@ int nq_dispatch_take(nq_dispatch* d, uint64_t* first, uint64_t* len) {
     }
   }
 }
+
+extern "C" {
 
 int nq_dispatch_reset(nq_dispatch* d) {
   if (!d) return set_error(NQ_ECONFIG, "null dispenser");

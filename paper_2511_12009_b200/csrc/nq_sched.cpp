@@ -387,7 +387,7 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
               continue;
             }
             uint64_t f = 0, l = 0;
-            const int got = nq_dispatch_take(disp, &f, &l);
+            const int got = dispatch_take_at_least(disp, low_water - (pub - consumed), &f, &l);
             if (got < 0) {
               fe = got;
               break;

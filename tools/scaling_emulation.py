@@ -33,13 +33,19 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
 
-def one(n, r, k, reps, mode):
+def one(n, r, k, reps, strategy):
     import numpy as np
     import torch
     from paper_2511_12009_b200 import nqueens as nq
     recs = nq.generate_packed(n, r)
+    strat = nq.PartitionStrategy[strategy]
+    weights = []
+    if strat is nq.PartitionStrategy.weighted:  # the paper's 8-GPU weights
+        w = list(nq.paper_gpu_weights)[:k]
+        weights = [x / sum(w) for x in w] if k <= 8 else []
+    chunk = 64 if strat is nq.PartitionStrategy.stealing else 0
     opts = nq.ExecuteOptions(config=nq.builtin_configs[0],
-                             plan=nq.PartitionPlan(nq.PartitionStrategy.guided, k, [], 0),
+                             plan=nq.PartitionPlan(strat, k, weights, chunk),
                              devices=[0] * k)
     dev = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).cuda()
     best = None
@@ -49,7 +55,8 @@ def one(n, r, k, reps, mode):
         if best is None or span < best[0]:
             best = (span, rep)
     span, rep = best
-    return {"k": k, "T_k_ms": span, "spans_ms": [round(w.span_ms, 2) for w in rep.workers],
+    return {"k": k, "strategy": strategy, "T_k_ms": span,
+            "spans_ms": [round(w.span_ms, 2) for w in rep.workers],
             "chunks": [w.chunks for w in rep.workers], "solutions": rep.total, "nodes": rep.nodes,
             "blocks_per_sm": int(os.environ.get("NQB_BLOCKS_PER_SM", "0"))}
 
@@ -61,10 +68,13 @@ def main():
     ap.add_argument("--ks", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--blocks", type=int, default=8, help="resident blocks per SM of one GPU")
+    ap.add_argument("--strategy", default="guided",
+                    choices=["guided", "stealing", "weighted", "uniform"],
+                    help="weighted = the reference's default plan with the paper's 8-GPU weights")
     ap.add_argument("--child", type=int, default=0)
     args = ap.parse_args()
     if args.child:
-        print(json.dumps(one(args.n, args.pre_rows, args.child, args.reps, "device")))
+        print(json.dumps(one(args.n, args.pre_rows, args.child, args.reps, args.strategy)))
         return
     t1 = None
     for k in [int(x) for x in args.ks.split(",")]:
@@ -75,7 +85,8 @@ def main():
         env = {**os.environ, "NQB_BLOCKS_PER_SM": str(max(1, args.blocks // k)),
                "CUDA_DEVICE_MAX_CONNECTIONS": "32"}
         out = subprocess.run([sys.executable, __file__, "--n", str(args.n), "--pre-rows",
-                              str(args.pre_rows), "--reps", str(args.reps), "--child", str(k)],
+                              str(args.pre_rows), "--reps", str(args.reps), "--child", str(k),
+                              "--strategy", args.strategy],
                              capture_output=True, text=True, env=env, check=True).stdout
         row = json.loads(out.strip().splitlines()[-1])
         if k == 1:
