@@ -285,6 +285,27 @@ def test_cancel_mid_run_stops_between_chunks():
     assert time.perf_counter() - t0 < 30
 
 
+def test_cancel_during_a_streaming_launch():
+    """Guided dispatch feeds ONE streaming launch; a cancel makes the feeder stop
+    publishing and close the queue: what was already published (at most about one guided
+    chunk) is counted, the rest is not, and the report says completed = False."""
+    import threading
+    import time
+    batch = nq.generate_packed(21, 7)                     # ~13 s of work on one B200
+    ev = threading.Event()
+    opts = nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.guided, 1))
+    assert nq.execute(12, 4, nq.ExecuteOptions(plan=opts.plan)).total == 14200  # warm
+    timer = threading.Timer(1.0, ev.set)
+    timer.start()
+    t0 = time.perf_counter()
+    rep = nq.execute_batch(21, 7, batch, opts)
+    dt = time.perf_counter() - t0
+    timer.cancel()
+    assert not rep.completed
+    assert 0 < rep.workers[0].processed < len(batch)
+    assert dt < 6.5, dt
+
+
 def test_cancel_inside_a_running_launch():
     """With the strided strategy each worker is ONE persistent launch; a cancel raised
     while it runs reaches the kernel through the device stop word (nq_ctx_set_cancel):
