@@ -141,3 +141,23 @@ def test_bench_single_process_multi_worker():
         assert line["n_gpus"] == 1 and line["config"]["solutions"] == Q[16]
         assert line["value"] > 1e10 and line["e2e"]["value"] > 0
         assert line["roofline"]["frac"] > 0
+
+
+@pytest.mark.parametrize("strategy", list(nq.PartitionStrategy))
+def test_empty_and_single_record_batches_every_strategy(strategy):
+    """Edge cases of the scheduler (test_scheduler.cpp:121-130): an empty batch counts 0
+    and completes; a single record (with a non-default multiplier) is counted once,
+    weighted, whatever the strategy and worker count."""
+    from paper_2511_12009_b200 import _lib
+    empty = np.zeros(0, dtype=_lib.SUB_DTYPE)
+    for workers in (1, 3):
+        o = nq.ExecuteOptions(config=nq.builtin_configs[0],
+                              plan=nq.PartitionPlan(strategy, workers, [], 16), devices=[0])
+        rep = nq.execute_batch(12, 4, empty, o)
+        assert rep.total == 0 and rep.completed and rep.nodes == 0
+        one = nq.generate_packed(12, 4)[100:101].copy()
+        want = nq.count_each(12, one, nq.KernelVariant.lastrow, pre_rows=4)[0][0]
+        one["row"] = (one["row"] & 0xFF) | (5 << 8)          # multiplier 5
+        rep = nq.execute_batch(12, 4, one, o)
+        assert rep.total == 5 * int(want) and rep.completed
+        assert sum(w.processed for w in rep.workers) == 1
