@@ -201,8 +201,9 @@ def run_reference_arm(args):
             "config": {"workload": f"N={args.n} R={args.pre_rows} full-frontier count",
                        "n": args.n, "pre_rows": args.pre_rows, "sample_stride": args.ref_stride,
                        "same_config": False,
-                       "why_sample": "the full count takes ~14 min on the host; the slice is a "
-                                     "systematic 1/%d sample of the same frontier" % args.ref_stride},
+                       "why_sample": "the full count would take ~%.0f min on these host cores; the "
+                                     "slice is a systematic 1/%d sample of the same frontier"
+                                     % (ms * args.ref_stride / 60000.0, args.ref_stride)},
             "cpu_baseline": {"value": v, "unit": "nodes/s", "cores": threads,
                              "cpu_model": cpu_model(), "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0,
