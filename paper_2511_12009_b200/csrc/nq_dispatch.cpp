@@ -171,6 +171,10 @@ int nq_dispatch_take(nq_dispatch* d, uint64_t* first, uint64_t* len) {
 // ceil(want / chunk) consecutive chunks in ONE step (one contiguous range, one queue
 // entry), the reference's granularity per take but not per queue entry: a chunk of 64
 // records per entry would make every lane walk thousands of entries per record.
+bool nqb200::dispatch_drained(const nq_dispatch* d) {
+  return d->s->taken.load(std::memory_order_relaxed) >= d->s->count;
+}
+
 int nqb200::dispatch_take_at_least(nq_dispatch* d, uint64_t want, uint64_t* first,
                                    uint64_t* len) {
   if (!d || !first || !len) return set_error(NQ_ECONFIG, "null dispenser argument");

@@ -91,6 +91,8 @@ uint64_t ctx_stream_published(const nq_ctx* c);
 // nq_dispatch_take for a streaming feeder that needs at least `want` records: stealing
 // returns ceil(want / chunk) consecutive chunks as one range (guided ignores `want`).
 int dispatch_take_at_least(nq_dispatch* d, uint64_t want, uint64_t* first, uint64_t* len);
+// Every record of the dispenser has been handed out (to any worker or process).
+bool dispatch_drained(const nq_dispatch* d);
 // Device-resident copy of a host batch on the context (ensure + H2D on its stream).
 int ctx_upload(nq_ctx* c, const nq_sub* host, uint64_t count, const nq_sub** dev);
 // Host roots deepened on the context's device to `target` rows (stream-ordered, the

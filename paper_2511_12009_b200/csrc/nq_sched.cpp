@@ -396,6 +396,9 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
             pushed.push_back(Pushed{pub, f, l});
             fe = ctx_stream_push(c, all + f, l);
             trace("published", f, l);
+            // nothing left anywhere: close at once, so that lanes waiting for more learn
+            // it now and start the tail donation instead of napping
+            if (fe == NQ_OK && dispatch_drained(disp)) break;
           }
           if (fe != NQ_OK) fe_msg = nq_last_error();
           ctx_stream_close(c, cancelled || fe != NQ_OK);
