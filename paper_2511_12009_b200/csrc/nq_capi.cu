@@ -140,7 +140,10 @@ struct nq_ctx {
   int* d_each_high = nullptr;
   size_t each_cap = 0;
   // [0] cursor, [1..5] totals, [6] stop word, [7] weighted-sum overflow flag,
-  // [8] streaming watchdog flag, [9] device mirror of the streaming publish word
+  // [8] streaming watchdog flag, [9] device mirror of the streaming publish word,
+  // [10] its bus-reader lock, [11..12] entries the bus reader copied into the device
+  // table and the end position of the last,
+  // [16..23] probe-build counters (NQB_STREAM_STATS)
   unsigned long long* d_ctl = nullptr;
   // pinned: [0..9] mirror of d_ctl, [10] stop source, [11] publish staging, [12] cursor read
   unsigned long long* h_ctl = nullptr;
@@ -191,20 +194,25 @@ int set_kernel_attributes(int device) {
   if (done[device]) return NQ_OK;
   int optin = 0;
   NQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  // dynamic limit = opt-in minus the kernel's static shared memory (the streaming
+  // kernels' per-warp queue state)
+  auto allow_smem = [optin](KernelFn fn) -> int {
+    cudaFuncAttributes fa{};
+    NQ_CUDA(cudaFuncGetAttributes(&fa, fn));
+    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - static_cast<int>(fa.sharedSizeBytes)));
+    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    return NQ_OK;
+  };
   for (int block : {64, 96, 128, 192, 256})
     for (bool per_sub : {false, true})
       for (int layout : {NQ_LAYOUT_V4, NQ_LAYOUT_PLANES}) {
         KernelFn fns[2] = {kernel_for(block, per_sub, layout), stream_kernel_for(block, layout)};
-        for (KernelFn fn : fns) {
-          NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-          NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        }
+        for (KernelFn fn : fns)
+          if (int rc = allow_smem(fn)) return rc;
       }
-  for (int k = 0; k < 3; ++k) {
-    KernelFn fn = wide_kernel(k == 1, k == 2);
-    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    NQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  }
+  for (int k = 0; k < 3; ++k)
+    if (int rc = allow_smem(wide_kernel(k == 1, k == 2))) return rc;
   done[device] = true;
   return NQ_OK;
 }
@@ -271,7 +279,7 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   Launch L;
   if (int rc = plan_launch(c, n, pre_rows, per_sub, &L)) return rc;
   if (!c->stream_open)
-    NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 10 * sizeof(unsigned long long), c->stream));
+    NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 24 * sizeof(unsigned long long), c->stream));
   DfsParams P{};
   P.subs = reinterpret_cast<const uint4*>(dev_subs);
   P.count = count;
@@ -293,6 +301,8 @@ int enqueue(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* dev_subs,
   P.q_pub = c->h_mbox;
   P.q_progress = c->h_mbox ? c->h_mbox + 1 : nullptr;
   P.q_pub_mirror = c->d_ctl + 9;
+  P.q_bus_lock = c->d_ctl + 10;
+  P.q_copied = c->d_ctl + 11;
   P.watchdog_ns = kQueueWatchdogNs;
   if (const char* e = std::getenv("NQB_STREAM_WATCHDOG_S"))
     P.watchdog_ns = static_cast<unsigned long long>(std::atof(e) * 1e9);
@@ -344,6 +354,15 @@ int finish(nq_ctx* c, int variant, bool h2d, int pre_rows, nq_result* out) {
     return set_error(NQ_ECUDA, "streaming launch: the host published nothing new for the "
                                 "watchdog period (NQB_STREAM_WATCHDOG_S, default 120 s); the "
                                 "launch gave up");
+#ifdef NQB_STREAM_STATS
+  {
+    unsigned long long st[8];
+    NQ_CUDA(cudaMemcpy(st, c->d_ctl + 16, sizeof(st), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "stream stats: rounds %llu pub_mirror %llu pub_host %llu entry %llu "
+                 "entry_host %llu naps %llu blocks %llu idle_lane_blocks %llu\n", st[0], st[1], st[2],
+                 st[3], st[4], st[5], st[6], st[7]);
+  }
+#endif
   nq_result r{};
   r.solutions = t[0];
   r.raw_solutions = t[1];
@@ -444,7 +463,7 @@ int ctx_stream_begin(nq_ctx* c, uint64_t max_chunks) {
     NQ_CUDA(cudaHostAlloc(&c->h_mbox, 2 * sizeof(unsigned long long), cudaHostAllocMapped));
   __atomic_store_n(&c->h_mbox[0], 0ull, __ATOMIC_RELEASE);
   __atomic_store_n(&c->h_mbox[1], 0ull, __ATOMIC_RELEASE);
-  NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 10 * sizeof(unsigned long long), c->stream));
+  NQ_CUDA(cudaMemsetAsync(c->d_ctl, 0, 24 * sizeof(unsigned long long), c->stream));
   NQ_CUDA(cudaMemsetAsync(c->d_tab, 0, max_chunks * sizeof(QChunk), c->stream));
   c->tab_n = 0;
   c->published = 0;
@@ -600,7 +619,7 @@ int nq_ctx_create(int device, nq_ctx** out) {
   NQ_CUDA(cudaEventCreate(&c->ev_k1));
   NQ_CUDA(cudaEventCreate(&c->ev_start));
   if (int rc = set_kernel_attributes(device)) return rc;
-  NQ_CUDA(cudaMalloc(&c->d_ctl, 16 * sizeof(unsigned long long)));
+  NQ_CUDA(cudaMalloc(&c->d_ctl, 24 * sizeof(unsigned long long)));
   NQ_CUDA(cudaMallocHost(&c->h_ctl, 16 * sizeof(unsigned long long)));
   *out = c.release();
   return NQ_OK;

@@ -22,8 +22,8 @@
 //     (C == 0), because POPC issues at 1/8 of the ALU rate on sm_100;
 //   * an idle lane holds C = 0, a = 0: every side effect is predicated off, so the
 //     idle check runs once per KSTEP steps;
-//   * per-lane u32 counters are folded into u64 totals at subproblem end and every
-//     2^15 K-step blocks, then warp-shuffle reduced with one atomicAdd per warp.
+//   * per-lane u32 counters are folded into u64 totals at subproblem end and before
+//     they reach 2^31, then warp-shuffle reduced with one atomicAdd per warp.
 //
 // Node accounting: one loop iteration places one queen at rows placed..n-1. The
 // reference's Alg. 3 settles row n-1 by popcount instead, so its iteration count is
@@ -66,7 +66,18 @@ struct DfsParams {
   const unsigned long long* q_pub;             // mapped host publish word
   unsigned long long* q_progress;              // mapped host: cursor, coarsely
   unsigned long long* q_pub_mirror;            // device: newest publish word any warp read
+  unsigned long long* q_bus_lock;              // device: held by the one warp reading q_pub
+  unsigned long long* q_copied;                // device: [entries copied into q_tab, their end]
   unsigned long long watchdog_ns;              // give up after this long without a publish
+};
+
+// A warp's view of the streaming queue (warp-uniform; in shared memory).
+struct WarpQueue {
+  unsigned long long pub_seen = 0ull;  // published positions as of the last read
+  unsigned long long end = 0ull;       // the current chunk entry: [base, end)
+  const uint4* base = nullptr;
+  uint32_t chunk = 0u;                 // its index in the table
+  uint32_t closed = 0u;                // the queue was closed at pub_seen
 };
 
 // One published chunk of a streaming launch (16-byte aligned: the device mirror is
@@ -264,21 +275,31 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
   int placed = 0, high = 0;
 
   bool exhausted = false;  // warp-uniform: no more records will be handed to this warp
-  uint32_t blocks = 0u;
   // streaming: this lane's queue position (taken from the cursor, possibly not yet
-  // published by the host) and a monotone hint into the chunk table
+  // published by the host)
   unsigned long long ticket = kNoTicket;
-  uint32_t chunk = 0u;
-  unsigned long long pub_seen = 0ull;  // warp-uniform: published positions last read
-  bool closed_seen = false;
+  // The warp-uniform queue state lives in shared memory, not in registers: it is only
+  // touched at refills, and seven more live registers across the step loop spill.
+  [[maybe_unused]] WarpQueue* wq = nullptr;
+  if constexpr (STREAM) {
+    __shared__ WarpQueue wq_s[BLOCK / 32];
+    wq = &wq_s[threadIdx.x >> 5];
+    *wq = WarpQueue{};  // every lane writes (and later reads) the same values
+  }
+#ifdef NQB_STREAM_STATS
+  // probe build only: [rounds, pub mirror reads, host pub reads, entry reads, host entry
+  // reads, naps, step blocks, idle lane-blocks] summed into totals[15..22]
+  unsigned long long st[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#define NQB_STAT(i) (++st[i])
+#else
+#define NQB_STAT(i) ((void)0)
+#endif
 
   // Starts record `idx` (reported as the failing index) at `rec` on this lane.
-  // Streaming chunks are copied in while the kernel runs, so their records are read
-  // through L2 (ld.global.cg), never from a possibly stale non-coherent line.
+  // Records are read-only for the launch's lifetime in both modes (a streaming launch
+  // only publishes ranges of a batch made device-resident before it started).
   auto start = [&](const uint4* rec, unsigned long long idx) {
-    uint4 s;
-    if constexpr (STREAM) s = __ldcg(rec);
-    else s = __ldg(rec);
+    const uint4 s = __ldg(rec);
     busy = true;
     weight = s.w >> 8;
     placed = static_cast<int>(s.w & 0xffu);
@@ -355,7 +376,13 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
           }
           continue;
         } else {
+        unsigned long long pub_seen = wq->pub_seen;  // published positions last read
+        bool closed_seen = wq->closed != 0u;
+        uint32_t chunk = wq->chunk;                  // chunk entry `chunk` is [w_base, w_end)
+        const uint4* w_base = wq->base;              // (w_end 0: none read yet)
+        unsigned long long w_end = wq->end;
         // Streaming: (1) idle lanes without a queue position take one from the cursor,
+        if (lane == 0u) NQB_STAT(0);
         const uint32_t need = __ballot_sync(0xffffffffu, a == 0u && ticket == kNoTicket);
         unsigned long long taken_end = 0ull;
         if (need) {
@@ -384,44 +411,90 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
           unsigned long long pw = 0ull;
           if (lane == __ffs(holders) - 1u) {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(pw) : "l"(P.q_pub_mirror) : "memory");
-            if ((pw & ~kQueueClosed) <= pub_seen && !(pw & kQueueClosed)) {
+            NQB_STAT(1);
+            // Stale mirror: one warp at a time reads the word over the bus. All warps
+            // cross a chunk boundary together (the cursor is shared); unserialised, their
+            // thousands of host reads queue up at the root complex (≈1 µs each). The
+            // reader also copies the newly published entries into the device table before
+            // it releases the new word, so the entries are never read over the bus again.
+            if ((pw & ~kQueueClosed) <= pub_seen && !(pw & kQueueClosed) &&
+                atomicCAS(P.q_bus_lock, 0ull, 1ull) == 0ull) {
+              __threadfence();
               unsigned long long ph;
+              NQB_STAT(2);
               asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(ph) : "l"(P.q_pub) : "memory");
               if (ph > pw) {
+                const unsigned long long target = ph & ~kQueueClosed;
+                // q_copied = {entries copied, end position of the last one}; every entry
+                // up to `target` was written before the word was released
+                volatile unsigned long long* cp = P.q_copied;
+                unsigned long long k = cp[0], done = cp[1];
+                while (done < target) {
+                  unsigned long long eb;
+                  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(done)
+                               : "l"(&P.q_host_tab[k].end) : "memory");
+                  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(eb)
+                               : "l"(&P.q_host_tab[k].base) : "memory");
+                  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + k), "l"(eb),
+                               "l"(done) : "memory");
+                  ++k;
+                }
+                cp[0] = k;
+                cp[1] = done;
                 asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(P.q_pub_mirror), "l"(ph)
                              : "memory");
                 pw = ph;
               }
+              __threadfence();
+              atomicExch(P.q_bus_lock, 0ull);
             }
           }
           pw = __shfl_sync(0xffffffffu, pw, __ffs(holders) - 1u);
           pub_seen = pw & ~kQueueClosed;
           closed_seen = (pw & kQueueClosed) != 0ull;
+          wq->pub_seen = pub_seen;
+          wq->closed = closed_seen ? 1u : 0u;
         }
-        if (ticket != kNoTicket) {
-          if (ticket < pub_seen) {
-            // chunk lookup: the device mirror, filled from the host table on a miss
-            unsigned long long eb, ee;
-            for (;; ++chunk) {  // tickets only grow: move to the entry holding this one
-              asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(eb), "=l"(ee)
-                           : "l"(P.q_tab + chunk) : "memory");
-              if (ee == 0ull) {  // first reader of this entry: fetch it from the host table
-                asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(eb)
-                             : "l"(&P.q_host_tab[chunk].base) : "memory");
-                asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(ee)
-                             : "l"(&P.q_host_tab[chunk].end) : "memory");
-                asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + chunk), "l"(eb),
-                             "l"(ee) : "memory");
-              }
-              if (ticket < ee) break;
-            }
+        // Published tickets become records. The chunk entry is warp-uniform (w_base,
+        // w_end of entry `chunk`): a warp's tickets are consecutive and only grow, so one
+        // lane reads the next entry (device table; read from the host table only if the
+        // bus reader above has not copied it yet, which its ordering rules out)
+        // only when the warp's tickets pass w_end — a few reads per chunk per warp, not
+        // one per record.
+        for (uint32_t res = __ballot_sync(0xffffffffu, ticket != kNoTicket && ticket < pub_seen);
+             res != 0u;) {
+          if (((res >> lane) & 1u) && ticket < w_end) {
             // expensive end of the chunk first, like the contiguous launch (reverse)
-            start(reinterpret_cast<const uint4*>(eb) + (ee - 1ull - ticket), ticket);
-            ticket = kNoTicket;
-          } else if (closed_seen) {
+            start(w_base + (w_end - 1ull - ticket), ticket);
             ticket = kNoTicket;
           }
+          res = __ballot_sync(0xffffffffu, ticket != kNoTicket && ticket < pub_seen);
+          if (res == 0u) break;
+          unsigned long long eb = 0ull, ee = 0ull;
+          if (lane == __ffs(res) - 1u) {
+            if (w_end != 0ull) ++chunk;
+            NQB_STAT(3);
+            asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(eb), "=l"(ee)
+                         : "l"(P.q_tab + chunk) : "memory");
+            if (ee == 0ull) {  // not copied yet: fetch it from the host table
+              NQB_STAT(4);
+              asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(eb)
+                           : "l"(&P.q_host_tab[chunk].base) : "memory");
+              asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(ee)
+                           : "l"(&P.q_host_tab[chunk].end) : "memory");
+              asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(P.q_tab + chunk), "l"(eb),
+                           "l"(ee) : "memory");
+            }
+          }
+          const uint32_t src = __ffs(res) - 1u;
+          chunk = __shfl_sync(0xffffffffu, chunk, src);
+          w_base = reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, eb, src));
+          w_end = __shfl_sync(0xffffffffu, ee, src);
+          wq->chunk = chunk;
+          wq->base = w_base;
+          wq->end = w_end;
         }
+        if (closed_seen && ticket != kNoTicket) ticket = kNoTicket;  // past the final count
         if (closed_seen && need && taken_end >= pub_seen) exhausted = true;
         // (3) positions still unpublished: step the busy lanes and look again after
         // KSTEP steps; if no lane has work, nap instead of spinning on the bus.
@@ -436,6 +509,7 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
             exhausted = true;
             break;
           }
+          if (lane == 0u) NQB_STAT(5);
           __nanosleep(1000);
           continue;
         }
@@ -490,6 +564,15 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
     }
 
     // ---- KSTEP predicated DFS steps -------------------------------------------------
+#ifdef NQB_STREAM_STATS
+    {
+      const uint32_t idle_now = __ballot_sync(0xffffffffu, a == 0u);
+      if (lane == 0u) {
+        NQB_STAT(6);
+        st[7] += __popc(idle_now);
+      }
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < KSTEP; ++k) {
       if constexpr (PER_SUB) {
@@ -500,8 +583,9 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
       dfs_step<STRIDE, LAYOUT, WIDE>(C, l, r, a, sp, sol, its);
     }
 
-    // Fold u32 counters periodically so they cannot wrap (≤ 2^15*KSTEP steps).
-    if (((++blocks) & 0x7fffu) == 0u) {
+    // Fold the u32 counters (lane-local) before they can wrap: its grows by at most
+    // KSTEP per block and sol <= its. No block counter: one register fewer.
+    if (its >= 0x80000000u) {
       const unsigned long long prod = static_cast<unsigned long long>(weight) * sol;
       tot_w += prod;
       wrapped |= tot_w < prod;
@@ -534,6 +618,14 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
     atomicAdd(P.totals + 2, tot_it);
     atomicAdd(P.totals + 3, tot_subs);
   }
+#ifdef NQB_STREAM_STATS
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long v = st[i];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0u && v) atomicAdd(P.totals + 15 + i, v);
+  }
+#endif
+#undef NQB_STAT
 }
 
 }  // namespace nqb200

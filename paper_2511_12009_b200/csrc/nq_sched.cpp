@@ -373,6 +373,13 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         int fe = NQ_OK;
         std::string fe_msg;  // nq_last_error() is per thread: carried back to this one
         std::thread feeder([&] {
+          // The lead of published-but-untaken records must outlast the feeder's own
+          // reaction time (~0.1 ms), whatever the record rate (N=18 R=7 takes 3 x 10^8
+          // records/s): it tracks the measured consumption rate, 300 us of it, never
+          // below lanes/8. A larger lead would only hold back work from other GPUs.
+          auto t_prev = clk::now();
+          uint64_t c_prev = 0;
+          double rate = 0.0;  // records per second, smoothed
           while (fe == NQ_OK && !launch_failed.load()) {
             if (cancel_raised(o.cancel)) {
               cancelled = true;
@@ -381,13 +388,23 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
             }
             uint64_t consumed = 0;
             ctx_stream_consumed(c, &consumed);
+            const auto now = clk::now();
+            const double dt = std::chrono::duration<double>(now - t_prev).count();
+            if (dt >= 200e-6) {
+              const double r = static_cast<double>(consumed - std::min(consumed, c_prev)) / dt;
+              rate = rate == 0.0 ? r : 0.7 * rate + 0.3 * r;
+              t_prev = now;
+              c_prev = consumed;
+            }
+            const uint64_t lead = std::max<uint64_t>(low_water, static_cast<uint64_t>(rate * 300e-6));
             const uint64_t pub = ctx_stream_published(c);
-            if (pub - consumed >= low_water) {
-              std::this_thread::sleep_for(std::chrono::microseconds(20));
+            if (pub - consumed >= lead) {
+              if (pub - consumed > 4 * lead) std::this_thread::sleep_for(std::chrono::microseconds(50));
+              else std::this_thread::yield();
               continue;
             }
             uint64_t f = 0, l = 0;
-            const int got = dispatch_take_at_least(disp, low_water - (pub - consumed), &f, &l);
+            const int got = dispatch_take_at_least(disp, lead - (pub - consumed), &f, &l);
             if (got < 0) {
               fe = got;
               break;
