@@ -8,9 +8,10 @@
 A step = one full count of the N=20 folded frontier (R=7: 22,781,426 packed records,
 1.865e12 DFS nodes) through the product's multi-GPU scheduler (execute_batch's
 counterpart, csrc/nq_sched.cpp): host-side GUIDED dynamic chunk dispatch (big chunks
-from the expensive end first, shrinking to the end), one host thread per GPU with two
-launches in flight, the persistent sm_100a DFS kernel, per-GPU u64 partials summed on
-the host with checked adds. No NCCL anywhere:
+from the expensive end first, shrinking to the end), one host thread per GPU feeding
+ONE persistent streaming launch of the sm_100a DFS kernel (one GPU alone: the whole
+frontier as one contiguous launch), per-GPU u64 partials summed on the host with
+checked adds. No NCCL anywhere:
   * one process (--gpus N, no torchrun): nq_solve_batch_device over devices 0..N-1;
   * torchrun (one process per GPU): every rank runs the same scheduler on its own GPU,
     all drawing chunks from ONE dispenser in POSIX shared memory (nq_dispatch_*), each
@@ -20,7 +21,7 @@ the host with checked adds. No NCCL anywhere:
 value  — frontier resident in HBM on every GPU (replicated, copied before timing), CUDA
          events: per GPU, first enqueued launch -> end of its last kernel; max over GPUs.
 e2e    — nq_solve_batch with the frontier in pinned HOST memory: one H2D of the frontier
-         per GPU, the streaming count, results D2H; host wall clock, max over ranks.
+         per GPU, the count, results D2H; host wall clock, max over ranks.
 roofline — integer-issue bound: achieved = per-GPU nodes/s x 18 algorithmic int ops per
            node vs the int-op peak measured live (nq_measure_int_peak).
 cpu_baseline — the reference's execute_batch (oracle/_ref/libnqref.so, built from the
@@ -413,7 +414,8 @@ def run_single_process(args):
                        "ms_per_step": sum(wall) / args.steps,
                        "call": f"nq_solve_batch (execute_batch) on the pinned host frontier, "
                                f"{args.dispatch} dispatch over {G} GPU(s): one H2D of the frontier "
-                               f"per GPU, streaming count, result read-back; host wall clock"}
+                               f"per GPU, {'streaming' if G > 1 else 'contiguous'} count, result "
+                               f"read-back; host wall clock"}
     if not args.no_execute:
         rep = None
         for _ in range(2):  # the first call also maps the stream-ordered pool; report the second
@@ -484,6 +486,9 @@ def base_line(args, n_gpus, value, t_dev, nodes_per_step, count, clk, launches, 
                    "solutions": OEIS.get(args.n), "nodes_per_step": nodes_per_step,
                    "parallelism": parallelism,
                    "dispatch": "single persistent launch" if args.single_launch else
+                               f"{args.dispatch} dispatch with one worker: the whole frontier as "
+                               f"one contiguous launch (expensive end first)" if n_gpus == 1 and
+                               os.environ.get("WORLD_SIZE", "1") == "1" else
                                f"{args.dispatch} host-side dynamic chunks fed into one streaming launch per GPU",
                    "l2": "flushed between steps (256 MiB write per GPU, untimed)"},
         "wall_ms": t_dev / args.steps,

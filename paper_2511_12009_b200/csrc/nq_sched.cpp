@@ -224,8 +224,15 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
   for (int w = 0; w < W; ++w)
     for (int v = 0; v < w; ++v) slot[w] += devs[v % G] == devs[w % G] ? 1 : 0;
 
+  // One worker with a private dispenser would take every chunk itself: it gets the
+  // contiguous launch instead (the same expensive-first order), without the streaming
+  // launch's refill and feeder cost (0.2-1%, profiles/r02_stream_probe.log).
+  const bool solo = W == 1 && !o.dispatch &&
+                    (o.strategy == NQ_PARTITION_STEALING || o.strategy == NQ_PARTITION_GUIDED);
   std::vector<uint64_t> ranges;
-  if (o.strategy == NQ_PARTITION_UNIFORM || o.strategy == NQ_PARTITION_WEIGHTED) {
+  if (solo) {
+    ranges = {0, count};
+  } else if (o.strategy == NQ_PARTITION_UNIFORM || o.strategy == NQ_PARTITION_WEIGHTED) {
     ranges.resize(2 * W);
     int rc;
     if (o.strategy == NQ_PARTITION_UNIFORM || !o.weights) {
@@ -240,7 +247,8 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
     }
     if (rc) return rc;
   }
-  const bool dynamic = o.strategy == NQ_PARTITION_STEALING || o.strategy == NQ_PARTITION_GUIDED;
+  const bool dynamic =
+      !solo && (o.strategy == NQ_PARTITION_STEALING || o.strategy == NQ_PARTITION_GUIDED);
   // Dynamic dispatch over roots deepened on the devices hands out ranges of the DEEPENED
   // stream (every worker deepens all roots; its records are in stream order).
   uint64_t disp_count = count;

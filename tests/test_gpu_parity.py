@@ -293,8 +293,10 @@ def test_cancel_during_a_streaming_launch():
     import time
     batch = nq.generate_packed(21, 7)                     # ~13 s of work on one B200
     ev = threading.Event()
-    opts = nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.guided, 1))
-    assert nq.execute(12, 4, nq.ExecuteOptions(plan=opts.plan)).total == 14200  # warm
+    # two workers (both on device 0): one worker alone gets the contiguous launch
+    opts = nq.ExecuteOptions(cancel=ev, plan=nq.PartitionPlan(nq.PartitionStrategy.guided, 2),
+                             devices=[0, 0])
+    assert nq.execute(12, 4, nq.ExecuteOptions(plan=opts.plan, devices=[0, 0])).total == 14200
     timer = threading.Timer(1.0, ev.set)
     timer.start()
     t0 = time.perf_counter()
@@ -302,7 +304,8 @@ def test_cancel_during_a_streaming_launch():
     dt = time.perf_counter() - t0
     timer.cancel()
     assert not rep.completed
-    assert 0 < rep.workers[0].processed < len(batch)
+    assert all(w.launches == 1 for w in rep.workers)
+    assert 0 < sum(w.processed for w in rep.workers) < len(batch)
     assert dt < 6.5, dt
 
 

@@ -30,7 +30,11 @@ def main():
     for _ in range(args.iters):
         if args.mode in ("both", "stream"):
             t0 = time.perf_counter()
+            # an explicit dispenser: one worker without one gets the contiguous launch
+            o.dispatch = nq.Dispatcher.create(len(recs), nq.PartitionStrategy.guided, 0, 1)
             rep = nq.execute_batch_device(args.n, args.pre_rows, [dev.data_ptr()], len(recs), o)
+            o.dispatch.close()
+            o.dispatch = None
             w = rep.workers[0]
             print(f"stream: kernel_ms {w.kernel_ms:.2f} span_ms {w.span_ms:.2f} "
                   f"wall {(time.perf_counter() - t0) * 1e3:.2f} chunks {w.chunks}", flush=True)
