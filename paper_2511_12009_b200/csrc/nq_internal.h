@@ -66,7 +66,8 @@ uint64_t ctx_last_expanded(const nq_ctx* c);
 
 // Asynchronous launch on a context (completed by nq_collect): host records (H2D into the
 // context's buffer), device-resident records, or host roots deepened to pre_rows on the
-// device first. The scheduler's workers keep two of these in flight on two contexts.
+// device first. The one-launch strategies' workers use one per worker; the dynamic ones
+// use the streaming form (ctx_stream_*).
 enum { kLaunchHost = 0, kLaunchDevice = 1, kLaunchExpand = 2 };
 int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, uint64_t count,
                int kind);

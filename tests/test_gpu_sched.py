@@ -2,7 +2,7 @@
 
 On a one-GPU box a device list that repeats device 0 (devices = [0, 0, 0, 0]) runs the
 whole multi-device code path — one host thread per worker, per-worker contexts, the
-dynamic dispenser, two launches in flight per worker, host checked sums — against one
+dynamic dispenser, one streaming launch per worker, host checked sums — against one
 device. Every total is compared with OEIS A000170 and every node count with Appendix B
 (independent pins: the reference generator's profile).
 """
