@@ -261,6 +261,27 @@ int check_args(int n, int pre_rows, int variant) {
   return NQ_OK;
 }
 
+// A page-locked (pinned) host batch is read in place by the kernel over the bus: each
+// 16-B record is read once, when a lane starts it, which costs nothing measurable even at
+// 3·10⁸ records/s (profiles/r02_zero_copy.log) — no H2D copy, no device buffer, and under
+// dynamic dispatch each GPU reads only the chunks it takes. Pageable memory is copied.
+// NQB_ZERO_COPY=0 forces the copy. Every host-pointer entry point is synchronous, so the
+// buffer is not released or changed while the kernel reads it.
+const nq_sub* mapped_records(const nq_sub* host) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("NQB_ZERO_COPY");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!enabled || !host) return nullptr;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, host) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+    return nullptr;
+  }
+  if (pa.type != cudaMemoryTypeHost || !pa.devicePointer) return nullptr;
+  return static_cast<const nq_sub*>(pa.devicePointer);
+}
+
 int ensure_capacity(nq_ctx* c, uint64_t count) {
   if (count <= c->d_cap) return NQ_OK;
   if (c->d_subs) cudaFree(c->d_subs);
@@ -393,12 +414,16 @@ int ctx_launch(nq_ctx* c, int n, int pre_rows, int variant, const nq_sub* subs, 
   c->last_bad = ~0ull;
   const nq_sub* dev = subs;
   if (kind == kLaunchHost) {
-    if (int rc = ensure_capacity(c, count)) return rc;
     NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
-    if (count)
-      NQ_CUDA(cudaMemcpyAsync(c->d_subs, subs, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
-                              c->stream));
-    dev = reinterpret_cast<const nq_sub*>(c->d_subs);
+    if (const nq_sub* m = mapped_records(subs)) {
+      dev = m;
+    } else {
+      if (int rc = ensure_capacity(c, count)) return rc;
+      if (count)
+        NQ_CUDA(cudaMemcpyAsync(c->d_subs, subs, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
+                                c->stream));
+      dev = reinterpret_cast<const nq_sub*>(c->d_subs);
+    }
   } else if (kind == kLaunchExpand) {
     // Only the coarse roots cross PCIe; the level buffers come from the device's
     // stream-ordered pool and are released on the same stream behind the kernel.
@@ -520,8 +545,12 @@ uint64_t ctx_stream_published(const nq_ctx* c) { return c->published; }
 
 int ctx_upload(nq_ctx* c, const nq_sub* host, uint64_t count, const nq_sub** dev) {
   NQ_CUDA(cudaSetDevice(c->device));
-  if (int rc = ensure_capacity(c, count)) return rc;
   NQ_CUDA(cudaEventRecord(c->ev_h2d, c->stream));
+  if (const nq_sub* m = mapped_records(host)) {
+    *dev = m;
+    return NQ_OK;
+  }
+  if (int rc = ensure_capacity(c, count)) return rc;
   if (count)
     NQ_CUDA(cudaMemcpyAsync(c->d_subs, host, count * sizeof(nq_sub), cudaMemcpyHostToDevice,
                             c->stream));

@@ -247,6 +247,42 @@ def test_empty_and_rejected_batches():
         assert "failed on subproblem 5" in str(e.value), (strategy, str(e.value))
 
 
+def test_pinned_host_batch_is_read_in_place(golden):
+    """A page-locked host batch is read by the kernel over the bus (no H2D copy); a
+    pageable one is copied. Same counts either way, through nq_count and through the
+    scheduler (two workers on device 0: streaming launches publishing host chunks), and
+    a malformed record in pinned memory is still rejected by index."""
+    import torch
+    n, r = 18, 6
+    recs = nq.generate_packed(n, r)
+    pinned = torch.from_numpy(recs.view(np.int32).reshape(-1, 4).copy()).pin_memory()
+    ctx = Ctx()
+    a = ctx.count(n, r, recs)                                  # pageable: copied
+    b = _lib.NqResult()
+    _lib.check(_lib.lib.nq_count(ctx.p, n, r, _lib.VARIANT_LASTROW,
+                                 ctypes.c_void_p(pinned.data_ptr()), len(recs), ctypes.byref(b)))
+    assert (a.solutions, a.nodes) == (b.solutions, b.nodes) == (golden["oeis_a000170"][n - 1], golden["appendix_b_nodes"][str(n)][str(r)])
+    assert a.h2d_ms > 1.0 and b.h2d_ms < 0.5, (a.h2d_ms, b.h2d_ms)
+    o = _lib.NqSolveOpts()
+    o.variant = _lib.VARIANT_LASTROW
+    o.strategy = _lib.PARTITION_GUIDED
+    o.worker_count = 2
+    devs = (ctypes.c_int * 2)(0, 0)
+    o.devices = devs
+    o.n_devices = 2
+    rep = _lib.NqReport()
+    _lib.check(_lib.lib.nq_solve_batch(n, r, ctypes.c_void_p(pinned.data_ptr()), len(recs),
+                                       ctypes.byref(o), ctypes.byref(rep)))
+    assert (rep.total, rep.nodes) == (golden["oeis_a000170"][n - 1], golden["appendix_b_nodes"][str(n)][str(r)])
+    bad = pinned.clone().pin_memory()
+    bad[7, 0] = int(np.int32(-1))                              # cols outside the board
+    with pytest.raises(_lib.NqError) as e:
+        _lib.check(_lib.lib.nq_count(ctx.p, n, r, _lib.VARIANT_LASTROW,
+                                     ctypes.c_void_p(bad.data_ptr()), len(recs), ctypes.byref(b)))
+    assert "record 7" in str(e.value)
+    ctx.close()
+
+
 def test_device_resident_async_path(oracle):
     import torch
     a = oracle.generate(16, 5)
