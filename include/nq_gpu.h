@@ -102,6 +102,9 @@ int nq_ctx_set_balance(nq_ctx* ctx, int donate);
 int nq_ctx_set_cancel(nq_ctx* ctx, const volatile int* cancel);
 
 /* Count a batch held in HOST memory (caller-owned, pageable or pinned). Synchronous.
+ * A pinned (page-locked) batch is read in place by the kernel over the bus, each record
+ * once (no copy; NQB_ZERO_COPY=0 disables this); a pageable one is copied first. The
+ * same holds for nq_solve_batch's host batch.
  * The GPU analogue of execute_batch's per-worker loop (scheduler.hpp:319-326).
  * pre_rows is the batch's pre-placement depth R: it sizes the shared-memory stack
  * (n-1-R frames, the Alg. 3 depth of stack_config.hpp:43-45); a record with fewer
