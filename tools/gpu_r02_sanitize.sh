@@ -1,6 +1,7 @@
 # compute-sanitizer on the round-2 streaming path: guided dispatch (one streaming launch
 # per worker fed through mapped host memory), with and without device deepening, and the
-# stealing feeder; plus the contiguous kernel as before.
+# stealing feeder; plus the contiguous kernel as before, and a pinned host batch read in
+# place by the kernel (zero-copy) through nq_count and two streaming workers.
 mkdir -p gpurun_out
 S=gpurun_out/r02_sanitize_summary.txt
 : > $S
@@ -16,6 +17,7 @@ for tool in memcheck racecheck synccheck; do
   run stealing $tool python -m paper_2511_12009_b200.cli solve --n 12 --pre-rows 4 --partition stealing --workers 2 --chunk-size 64
 done
 for tool in memcheck racecheck; do
+  run pinned $tool python -m pytest -q -m gpu tests/test_gpu_parity.py -k pinned_host
   NQB_DEVICE_EXPAND_MIN_RECORDS=0 run guided_deepen $tool python -m paper_2511_12009_b200.cli solve --n 13 --pre-rows 6 --partition guided --workers 2
 done
 cat $S
