@@ -492,8 +492,11 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
           }
         } else if (!ranges.empty()) {
           const uint64_t first = ranges[2 * w], len = ranges[2 * w + 1] - first;
-          st.assigned = len;
-          emit(o, NQ_LOG_START, w, len, count ? double(len) / double(count) : 0.0);
+          // a lone dynamic worker reports like the reference's stealing worker
+          // (assigned 0 = dynamic, scheduler.hpp:106, :350)
+          st.assigned = solo ? 0 : len;
+          emit(o, NQ_LOG_START, w, solo ? 0 : len,
+               solo || !count ? 0.0 : double(len) / double(count));
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
           } else if (len) {

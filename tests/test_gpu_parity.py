@@ -146,6 +146,8 @@ def test_totals_invariant_across_strategies_and_workers():
             assert sum(w.partial_sum for w in rep.workers) == rep.total
             if strategy in (nq.PartitionStrategy.uniform, nq.PartitionStrategy.weighted):
                 assert sum(w.assigned for w in rep.workers) == rep.task_count
+            if strategy in (nq.PartitionStrategy.stealing, nq.PartitionStrategy.guided):
+                assert all(w.assigned == 0 for w in rep.workers)  # 0 = dynamic (:106)
 
 
 def test_kernel_flag_same_totals():
