@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
   if constexpr (STREAM) {
     __shared__ WarpQueue wq_s[BLOCK / 32];
     wq = &wq_s[threadIdx.x >> 5];
-    *wq = WarpQueue{};  // every lane writes (and later reads) the same values
+    if (lane == 0u) *wq = WarpQueue{};  // lane 0 writes, __syncwarp publishes to the warp
+    __syncwarp();
   }
 #ifdef NQB_STREAM_STATS
   // probe build only: [rounds, pub mirror reads, host pub reads, entry reads, host entry
@@ -452,8 +453,12 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
           pw = __shfl_sync(0xffffffffu, pw, __ffs(holders) - 1u);
           pub_seen = pw & ~kQueueClosed;
           closed_seen = (pw & kQueueClosed) != 0ull;
-          wq->pub_seen = pub_seen;
-          wq->closed = closed_seen ? 1u : 0u;
+          __syncwarp();  // every lane's read of the view above is done
+          if (lane == 0u) {
+            wq->pub_seen = pub_seen;
+            wq->closed = closed_seen ? 1u : 0u;
+          }
+          __syncwarp();
         }
         // Published tickets become records. The chunk entry is warp-uniform (w_base,
         // w_end of entry `chunk`): a warp's tickets are consecutive and only grow, so one
@@ -490,9 +495,13 @@ __global__ void __launch_bounds__(BLOCK, 1152 / BLOCK) nq_dfs_kernel(DfsParams P
           chunk = __shfl_sync(0xffffffffu, chunk, src);
           w_base = reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, eb, src));
           w_end = __shfl_sync(0xffffffffu, ee, src);
-          wq->chunk = chunk;
-          wq->base = w_base;
-          wq->end = w_end;
+          __syncwarp();
+          if (lane == 0u) {
+            wq->chunk = chunk;
+            wq->base = w_base;
+            wq->end = w_end;
+          }
+          __syncwarp();
         }
         if (closed_seen && ticket != kNoTicket) ticket = kNoTicket;  // past the final count
         if (closed_seen && need && taken_end >= pub_seen) exhausted = true;

@@ -17,7 +17,7 @@ for tool in memcheck racecheck synccheck; do
   run stealing $tool python -m paper_2511_12009_b200.cli solve --n 12 --pre-rows 4 --partition stealing --workers 2 --chunk-size 64
 done
 for tool in memcheck racecheck; do
-  run pinned $tool python -m pytest -q -m gpu tests/test_gpu_parity.py -k pinned_host
+  run pinned $tool python tools/pinned_smoke.py
   NQB_DEVICE_EXPAND_MIN_RECORDS=0 run guided_deepen $tool python -m paper_2511_12009_b200.cli solve --n 13 --pre-rows 6 --partition guided --workers 2
 done
 cat $S
