@@ -1,0 +1,58 @@
+#!/usr/bin/env python3
+"""Per-N table on one B200 through the product call a user makes (nqueens.execute: host
+frontier or device-side deepening, guided dispatch, the sm_100a DFS kernel): wall time,
+Alg. 3 DFS nodes/s, fraction of the integer roofline (18 int ops per node against the
+LOP3+IMAD int32 peak measured live on this GPU), every count checked against OEIS
+A000170. One JSON line per N.
+
+    python tools/per_n.py --ns 16,17,18,19,20,21,22 [--reps 2]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+OEIS = {16: 14772512, 17: 95815104, 18: 666090624, 19: 4968057848, 20: 39029188884,
+        21: 314666222712, 22: 2691008701644, 23: 24233937684440}
+INT_OPS_PER_NODE = 18
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ns", default="16,17,18,19,20,21,22")
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args()
+    from paper_2511_12009_b200 import nqueens as nq
+    peak, mhz = nq.measure_int_peak(0)
+    nq.execute(12, 4, nq.ExecuteOptions())  # context, module and pool warm
+    for n in [int(x) for x in args.ns.split(",")]:
+        r = 6 if n <= 18 else 7
+        best = None
+        for _ in range(args.reps if n <= 21 else 1):
+            t0 = time.perf_counter()
+            rep = nq.execute(n, r, nq.ExecuteOptions(devices=[0]))
+            wall = (time.perf_counter() - t0) * 1e3
+            if rep.total != OEIS[n]:
+                raise SystemExit(f"N={n}: {rep.total} != OEIS {OEIS[n]}")
+            if best is None or wall < best[0]:
+                best = (wall, rep)
+        wall, rep = best
+        nps = rep.nodes / (wall / 1e3)
+        print(json.dumps({
+            "n": n, "pre_rows": r, "solutions": rep.total, "oeis_ok": True,
+            "subproblems": rep.task_count, "nodes": rep.nodes, "wall_ms": round(wall, 2),
+            "calc_ms": round(rep.calc_ms, 2), "generation_ms": round(rep.generation_ms, 2),
+            "kernel_span_ms": round(max(w.span_ms for w in rep.workers), 2),
+            "nodes_per_s": nps, "int_roofline_frac": nps * INT_OPS_PER_NODE / peak,
+            "int_peak_ops_per_s": peak, "sm_mhz_at_peak_probe": mhz,
+            "call": "nqueens.execute(n, R, ExecuteOptions(devices=[0])) — guided, 1 GPU"}),
+            flush=True)
+
+
+if __name__ == "__main__":
+    main()
