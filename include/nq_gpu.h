@@ -264,7 +264,8 @@ int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_report* out);
 int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* dev_subs, uint64_t count,
                           const nq_solve_opts* opts, nq_report* out);
 /* execute_batch over host ROOTS that each worker deepens to target_rows on its device
- * before counting (only the roots cross PCIe; strided or guided). The totals equal
+ * before counting (only the roots cross PCIe; strided or guided, or any strategy with
+ * one worker). The totals equal
  * execute_batch over the deepened records; report.workers[].processed counts deepened
  * records. This is how execute() runs large frontiers and how a systematic slice of
  * the N=27 R=7 frontier is cut into GPU-sized records for the projection. */

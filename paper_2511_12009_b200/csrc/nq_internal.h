@@ -107,8 +107,10 @@ uint64_t ctx_lanes(nq_ctx* c, int n, int pre_rows);  // resident lanes of a laun
 // (target_rows == 0: count the records as they are). nq_solve_batch is the
 // target_rows == 0 case; nq_solve uses the deepening form for large frontiers.
 // dev_subs (optional): per worker-device full copies of subs already on the devices.
+// deep_total (optional, 0 = unknown): the number of deepened records, reported as a lone
+// range worker's assignment (what the reference's execute would have handed it).
 int solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs,
                      const nq_sub* const* dev_subs, uint64_t count, const nq_solve_opts* opts,
-                     nq_report* out);
+                     nq_report* out, uint64_t deep_total = 0);
 
 }  // namespace nqb200

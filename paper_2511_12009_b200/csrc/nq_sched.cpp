@@ -167,7 +167,7 @@ extern "C" int nq_solve_batch_device(int n, int pre_rows, const nq_sub* const* d
 
 int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub* subs,
                              const nq_sub* const* dev_subs, uint64_t count,
-                             const nq_solve_opts* opts, nq_report* out) {
+                             const nq_solve_opts* opts, nq_report* out, uint64_t deep_total) {
   using clk = std::chrono::steady_clock;
   // The pooled per-device contexts are shared by every call: concurrent calls from
   // different host threads run one after the other (the reference's execute_batch is
@@ -195,8 +195,6 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
                                 target_rows ? target_rows : pre_rows,
                                 o.variant == NQ_VARIANT_LASTROW))
     return rc;
-  if (target_rows && o.strategy != NQ_PARTITION_STRIDED && o.strategy != NQ_PARTITION_GUIDED)
-    return set_error(NQ_ECONFIG, "device-side deepening needs the strided or guided strategy");
   if (dev_subs && o.strategy == NQ_PARTITION_STRIDED)
     return set_error(NQ_ECONFIG, "a device-resident frontier is split by ranges or chunks "
                                  "(uniform, weighted, stealing, guided), not strided");
@@ -217,6 +215,12 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
   const int W = o.worker_count > 0 ? o.worker_count : G;
   if (W > NQ_MAX_WORKERS)
     return set_error(NQ_ECONFIG, "worker_count above " + std::to_string(NQ_MAX_WORKERS));
+  // Deepened records exist only on the devices: one worker may take its roots as one
+  // range under any strategy; several need strided shares or guided chunks of them.
+  if (target_rows && W > 1 && o.strategy != NQ_PARTITION_STRIDED &&
+      o.strategy != NQ_PARTITION_GUIDED)
+    return set_error(NQ_ECONFIG, "device-side deepening over several workers needs the "
+                                 "strided or guided strategy");
   // Worker w runs on devs[w % G]. Its context slot is the number of earlier workers on
   // the same device id, so two workers never share a context (stream, buffers, result
   // mirror) even when the device list repeats a device (devices = {0, 0, ...}).
@@ -493,9 +497,11 @@ int nqb200::solve_batch_impl(int n, int pre_rows, int target_rows, const nq_sub*
         } else if (!ranges.empty()) {
           const uint64_t first = ranges[2 * w], len = ranges[2 * w + 1] - first;
           // a lone dynamic worker reports like the reference's stealing worker
-          // (assigned 0 = dynamic, scheduler.hpp:106, :350)
-          st.assigned = solo ? 0 : len;
-          emit(o, NQ_LOG_START, w, solo ? 0 : len,
+          // (assigned 0 = dynamic, scheduler.hpp:106, :350); a lone range worker over
+          // deepened roots reports the deepened records it was handed (:330)
+          const uint64_t shown = deep_total && W == 1 ? deep_total : len;
+          st.assigned = solo ? 0 : shown;
+          emit(o, NQ_LOG_START, w, solo ? 0 : shown,
                solo || !count ? 0.0 : double(len) / double(count));
           if (cancel_raised(o.cancel)) {
             interrupted.store(true);
@@ -578,8 +584,16 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
   uint64_t expand_min = 1ull << 20;
   if (const char* e = std::getenv("NQB_DEVICE_EXPAND_MIN_RECORDS")) expand_min = std::strtoull(e, nullptr, 10);
   const int coarse = std::max(2, pre_rows - 3);
-  const bool deepenable = o.strategy == NQ_PARTITION_STRIDED ||
-                          (o.strategy == NQ_PARTITION_GUIDED && !o.dispatch);
+  // One worker (the reference's default plan: weighted, worker_count 1) takes the whole
+  // frontier under any strategy, so it can always be deepened on its device.
+  int ndev = 0;
+  if (nq_device_count(&ndev) != NQ_OK) ndev = 0;
+  const int n_dev = o.devices && o.n_devices > 0 ? o.n_devices
+                    : o.n_devices > 0           ? std::min(o.n_devices, ndev)
+                                                : ndev;
+  const bool one_worker = (o.worker_count > 0 ? o.worker_count : n_dev) == 1;
+  const bool deepenable = !o.dispatch && (o.strategy == NQ_PARTITION_STRIDED ||
+                                          o.strategy == NQ_PARTITION_GUIDED || one_worker);
   if (total >= expand_min && deepenable && coarse < pre_rows) {
     uint64_t roots_n = 0;
     if (int rc = count_subproblems(n, coarse, &roots_n)) return rc;
@@ -587,7 +601,8 @@ extern "C" int nq_solve(int n, int pre_rows, const nq_solve_opts* opts, nq_repor
     if (int rc = generate_slice(n, coarse, 1, 0, roots.data(), roots_n, &roots_n)) return rc;
     const double gen_ms = std::chrono::duration<double, std::milli>(clk::now() - g0).count();
     emit(o, NQ_LOG_GENERATION, 0, total, gen_ms);
-    const int rc = solve_batch_impl(n, coarse, pre_rows, roots.data(), nullptr, roots_n, &o, out);
+    const int rc =
+        solve_batch_impl(n, coarse, pre_rows, roots.data(), nullptr, roots_n, &o, out, total);
     if (rc) return rc;
     out->task_count = total;
     out->generation_ms = gen_ms;

@@ -460,6 +460,30 @@ def test_execute_deepens_large_frontiers_on_the_device(monkeypatch, golden):
     assert nq.execute(16, 6, nq.ExecuteOptions(plan=nq.PartitionPlan(nq.PartitionStrategy.strided, 1))).total == 14772512
 
 
+def test_one_worker_plans_deepen_on_the_device(monkeypatch, golden):
+    """With ONE worker every strategy (the reference's default plan is weighted with one
+    worker) takes the device-deepening path, and the report and log lines keep the
+    reference's semantics: a range worker is assigned the whole R-frontier
+    (scheduler.hpp:330, :336-340), a stealing worker 0 (:106, :350)."""
+    monkeypatch.setenv("NQB_DEVICE_EXPAND_MIN_RECORDS", "1000")
+    total = nq.count_subproblems(16, 6)
+    for strategy in (nq.PartitionStrategy.weighted, nq.PartitionStrategy.uniform,
+                     nq.PartitionStrategy.stealing):
+        lines = []
+        opts = nq.ExecuteOptions(plan=nq.PartitionPlan(strategy, 1, [], 64), log=lines.append)
+        rep = nq.execute(16, 6, opts)
+        assert rep.completed and rep.total == 14772512
+        assert rep.nodes == golden["appendix_b_nodes"]["16"]["6"]
+        assert rep.task_count == total and rep.workers[0].processed == total
+        start = [x for x in lines if "start job" in x]
+        assert len(start) == 1
+        if strategy is nq.PartitionStrategy.stealing:
+            assert rep.workers[0].assigned == 0 and "with 0(0.00) subproblems" in start[0]
+        else:
+            assert rep.workers[0].assigned == total
+            assert f"with {total}(1.00) subproblems" in start[0], start[0]
+
+
 def test_bench_samples_rederived_on_device():
     """The CPU-baseline slices bench.py times (tests/golden/bench_samples.json, pinned
     with the C oracle) give the same weighted total and node count on the GPU."""
