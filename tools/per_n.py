@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
-"""Per-N table on one B200 through the product call a user makes (nqueens.execute: host
-frontier or device-side deepening, guided dispatch, the sm_100a DFS kernel): wall time,
+"""Per-N table on one B200 through the product call a user makes (nqueens.execute with the
+reference's default plan — weighted, one worker: host frontier below 2^20 records, else
+deepened on the device — and the sm_100a DFS kernel): wall time,
 Alg. 3 DFS nodes/s, fraction of the integer roofline (18 int ops per node against the
 LOP3+IMAD int32 peak measured live on this GPU), every count checked against OEIS
 A000170. One JSON line per N.
@@ -50,7 +51,7 @@ def main():
             "kernel_span_ms": round(max(w.span_ms for w in rep.workers), 2),
             "nodes_per_s": nps, "int_roofline_frac": nps * INT_OPS_PER_NODE / peak,
             "int_peak_ops_per_s": peak, "sm_mhz_at_peak_probe": mhz,
-            "call": "nqueens.execute(n, R, ExecuteOptions(devices=[0])) — guided, 1 GPU"}),
+            "call": "nqueens.execute(n, R, ExecuteOptions(devices=[0])) — default plan (weighted, 1 worker), 1 GPU"}),
             flush=True)
 
 
