@@ -6,11 +6,12 @@
 // failure rethrown after join, and a checked final sum. Here the same W workers each
 // drive one device stream (worker w -> devices[w % G], own pooled context) and hand
 // whole ranges / chunks to the persistent DFS kernel instead of one subproblem at a
-// time. Two GPU strategies are added: STRIDED (the default) deals record i to worker
-// i mod W and runs each worker's share as ONE persistent launch — the cost of a record
-// rises with its index, so striding balances workers statistically and
-// every device pays one tail instead of one per chunk; GUIDED hands out chunks that
-// shrink as the stream drains, from the expensive end first.
+// time. Two GPU strategies are added: GUIDED (the default) hands out chunks that
+// shrink as the stream drains, from the expensive end first (the cost of a record rises
+// with its index), and each device runs ONE streaming launch that the
+// host feeds chunk by chunk (nq_dispatch.cpp); STRIDED deals record i to worker i mod W
+// and runs each worker's share as one persistent launch, which balances the workers
+// statistically with no host traffic while the kernels run.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
