@@ -628,7 +628,11 @@ int nq_ctx_create(int device, nq_ctx** out) {
   if (device < 0 || device >= ndev)
     return set_error(NQ_ECUDA, "device " + std::to_string(device) + " not present (" +
                                    std::to_string(ndev) + " visible)");
-  std::unique_ptr<nq_ctx> c(new nq_ctx);
+  // a context that fails half-way is released with everything it created so far
+  struct CtxDeleter {
+    void operator()(nq_ctx* x) const { nq_ctx_destroy(x); }
+  };
+  std::unique_ptr<nq_ctx, CtxDeleter> c(new nq_ctx);
   c->device = device;
   NQ_CUDA(cudaSetDevice(device));
   cudaDeviceProp prop;
